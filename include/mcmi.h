@@ -1,0 +1,168 @@
+/* include/mcmi.h — C-ABI of the B200 MCMCMI preconditioner builder.
+ *
+ * Drop-in boundary for the reference's preconditioner-build path:
+ *
+ *   mcspai::ApproxInverse mcspai::compute_preconditioner(const CsrMatrix& b,
+ *                                                        const McConfig& cfg,
+ *                                                        int n_threads = 0);
+ *   (/root/reference/proj/include/mcspai/mc_engine.hpp:80-81,
+ *    implementation src/mc_engine.cpp:153-233)
+ *
+ * The reference passes std::vector-backed CSR (int64 indices, f64 values,
+ * csr.hpp:10-21) by const reference and returns the result by value.  A C ABI
+ * cannot return an unknown-size value, so the host entry point returns an
+ * opaque result handle: build -> query sizes -> copy out -> free
+ * (mcmi_build / mcmi_result_sizes / mcmi_result_copy / mcmi_result_free).
+ * Reference exceptions map to status codes (see MCMI_E*); the message text is
+ * the reference's own (mc_engine.cpp:14, split.cpp:48,68,95, csr.cpp:129).
+ * include/mcmi/mcspai_compat.hpp re-throws them as the same C++ types.
+ *
+ * The device-resident engine (mcmi_engine_*) is the same pipeline with inputs
+ * and outputs in HBM, used for sharded multi-GPU builds and for timing.
+ *
+ * All entry points are reentrant; one engine must not be used by two host
+ * threads at once.
+ */
+#ifndef MCMI_H
+#define MCMI_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MCMI_ABI_VERSION 1
+
+/* status codes */
+#define MCMI_OK 0
+#define MCMI_EINVAL 1  /* std::invalid_argument (drop fraction, alpha, ||A|| range, bad config) */
+#define MCMI_ESPLIT 2  /* mcspai::SplitError (degenerate diagonal, dominance failure) */
+#define MCMI_ERANGE 3  /* std::out_of_range (column index outside [0, n)) */
+#define MCMI_ECUDA 4   /* CUDA runtime failure */
+#define MCMI_ENOMEM 5  /* device or host allocation failure */
+#define MCMI_ENODEV 6  /* no CUDA device / device ordinal invalid */
+
+/* AugmentationMode (split.hpp:9-12) */
+#define MCMI_AUGMENT_PLAIN 0
+#define MCMI_AUGMENT_SIGN_AWARE 1
+/* DropMode (csr.hpp:61-64) */
+#define MCMI_DROP_VALUE_RANGE 0
+#define MCMI_DROP_COUNT_QUANTILE 1
+/* RNG keying of the walks */
+#define MCMI_RNG_REFERENCE 0 /* RngStream(seed, row), draws numbered across chains:
+                                byte-identical to the reference (mc_engine.cpp:168) */
+#define MCMI_RNG_KEYED 1     /* u(row, chain, step) = Philox({step>>1, chain, row}, seed) */
+
+/* Mirror of mcspai::McConfig (mc_engine.hpp:15-26).  std::optional fields are
+ * split into has_* flags; every int64 value is meaningful, as in the reference. */
+typedef struct mcmi_config {
+    double epsilon;       /* default 0.0625 */
+    double delta;         /* default 0.0625 */
+    double alpha;         /* default 5.0 */
+    int32_t mode;         /* MCMI_AUGMENT_*, default sign_aware */
+    int32_t drop_mode;    /* MCMI_DROP_*, default value_range */
+    double drop_fraction; /* default 0.0 */
+    int64_t retain_k;     /* 0 = unlimited */
+    int32_t has_chains_override;
+    int32_t has_max_len_override;
+    int64_t chains_override;
+    int64_t max_len_override;
+    uint64_t master_seed;
+    int32_t rng_mode; /* MCMI_RNG_*, default MCMI_RNG_REFERENCE */
+    int32_t device;   /* CUDA device ordinal for mcmi_build */
+} mcmi_config;
+
+/* Fills cfg with the reference defaults (McConfig{}). */
+void mcmi_config_default(mcmi_config* cfg);
+
+/* Square CSR in the reference layout (csr.hpp:16-21): row_ptr[n+1],
+ * col_idx[nnz], values[nnz], nnz = row_ptr[n].  Host pointers for mcmi_build,
+ * device pointers for mcmi_engine_build. */
+typedef struct mcmi_csr_view {
+    int64_t n;
+    const int64_t* row_ptr;
+    const int64_t* col_idx;
+    const double* values;
+} mcmi_csr_view;
+
+/* Per-build statistics (not in the reference; budget_echo is ChainBudget,
+ * mc_engine.hpp:28-31). */
+typedef struct mcmi_stats {
+    int64_t n_chains;     /* ChainBudget::n_chains */
+    int64_t max_len;      /* ChainBudget::max_len */
+    double a_norm;        /* SplitSystem::a_norm */
+    int64_t rows;         /* rows built (row_end - row_begin) */
+    int64_t nnz;          /* entries of the built rows of M */
+    int64_t walk_steps;   /* sampled transitions (one per s->t move) */
+    int64_t walk_deg_sum; /* sum over steps of deg(s): algorithmic bytes = 20*steps + 8*deg_sum */
+    int64_t hash_cap;     /* accumulator capacity of the first tier */
+    int64_t rows_retried; /* rows re-run on a larger accumulator tier */
+    double ms_tables;     /* device time: drop + split + transition tables */
+    double ms_walk;       /* device time: walk + accumulate + finalize kernels */
+    double ms_assemble;   /* device time: row-pointer scan + CSR compaction */
+    double ms_total;      /* device time of the whole build (excl. host copies) */
+    int64_t launches;     /* kernels launched by this build */
+    double ms_walk_kernel; /* device time of the walk kernel launches alone */
+} mcmi_stats;
+
+/* ------------------------------------------------------------ host API */
+
+typedef struct mcmi_result mcmi_result;
+
+/* compute_preconditioner: host CSR in, host result out (H2D/D2H inside). */
+int mcmi_build(const mcmi_csr_view* b, const mcmi_config* cfg, mcmi_result** out, char* err,
+               size_t errlen);
+/* Same, restricted to rows [row_begin, row_end) of M (a row shard: the
+ * result's row_ptr starts at 0, RowMeta covers only those rows).  The
+ * transition tables always cover all n states. */
+int mcmi_build_rows(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_begin,
+                    int64_t row_end, mcmi_result** out, char* err, size_t errlen);
+int mcmi_result_sizes(const mcmi_result* r, int64_t* n, int64_t* nnz);
+/* Any pointer may be NULL.  row_ptr[n+1], col_idx[nnz], values[nnz],
+ * chains_used[n] / entries_before[n] = RowMeta (mc_engine.hpp:33-36),
+ * n_chains / max_len = budget_echo. */
+int mcmi_result_copy(const mcmi_result* r, int64_t* row_ptr, int64_t* col_idx, double* values,
+                     int64_t* chains_used, int64_t* entries_before, int64_t* n_chains,
+                     int64_t* max_len);
+int mcmi_result_stats(const mcmi_result* r, mcmi_stats* stats);
+void mcmi_result_free(mcmi_result* r);
+
+/* ---------------------------------------------------- device-resident API */
+
+typedef struct mcmi_engine mcmi_engine;
+
+/* Device CSR shard produced by mcmi_engine_build; pointers are owned by the
+ * engine and stay valid until the next build or destroy. */
+typedef struct mcmi_device_csr {
+    int64_t row_begin, row_end; /* global rows [row_begin, row_end) */
+    int64_t nnz;
+    int64_t* row_ptr;        /* [rows+1], starts at 0 */
+    int64_t* col_idx;        /* [nnz] */
+    double* values;          /* [nnz] */
+    int64_t* chains_used;    /* [rows] */
+    int64_t* entries_before; /* [rows] */
+} mcmi_device_csr;
+
+int mcmi_engine_create(int device, mcmi_engine** out, char* err, size_t errlen);
+void mcmi_engine_destroy(mcmi_engine* e);
+/* Builds rows [row_begin, row_end) of M from a device-resident B on `stream`
+ * (a cudaStream_t; NULL = the engine's own stream).  Synchronises with the
+ * stream once after the transition tables (the chain budget is derived on the
+ * host with glibc log/ceil, mc_engine.cpp:12-33) and once at the end. */
+int mcmi_engine_build(mcmi_engine* e, const mcmi_csr_view* b_dev, const mcmi_config* cfg,
+                      int64_t row_begin, int64_t row_end, void* stream, mcmi_device_csr* out,
+                      mcmi_stats* stats, char* err, size_t errlen);
+
+/* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream): copies an
+ * engine output into caller-owned host or device memory. */
+int mcmi_copy(void* dst, const void* src, size_t bytes, void* stream);
+
+/* Library identification: returns "mcmi <abi> sm_100a". */
+const char* mcmi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,119 @@
+"""ctypes binding of the C-ABI in include/mcmi.h (libmcmi.so, sm_100a).
+
+The product path has no CPU fallback: if the library is missing this module
+raises, and every call that cannot reach a B200 returns an error status.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+from .build import LIB
+
+_i64p = C.POINTER(C.c_int64)
+_f64p = C.POINTER(C.c_double)
+
+MCMI_OK, MCMI_EINVAL, MCMI_ESPLIT, MCMI_ERANGE, MCMI_ECUDA, MCMI_ENOMEM, MCMI_ENODEV = range(7)
+
+#: every symbol include/mcmi.h declares
+EXPORTS = [
+    "mcmi_config_default", "mcmi_build", "mcmi_build_rows", "mcmi_result_sizes", "mcmi_result_copy",
+    "mcmi_result_stats", "mcmi_result_free", "mcmi_engine_create", "mcmi_engine_destroy",
+    "mcmi_engine_build", "mcmi_copy", "mcmi_version",
+]
+
+
+class mcmi_config(C.Structure):
+    _fields_ = [
+        ("epsilon", C.c_double),
+        ("delta", C.c_double),
+        ("alpha", C.c_double),
+        ("mode", C.c_int32),
+        ("drop_mode", C.c_int32),
+        ("drop_fraction", C.c_double),
+        ("retain_k", C.c_int64),
+        ("has_chains_override", C.c_int32),
+        ("has_max_len_override", C.c_int32),
+        ("chains_override", C.c_int64),
+        ("max_len_override", C.c_int64),
+        ("master_seed", C.c_uint64),
+        ("rng_mode", C.c_int32),
+        ("device", C.c_int32),
+    ]
+
+
+class mcmi_csr_view(C.Structure):
+    _fields_ = [("n", C.c_int64), ("row_ptr", C.c_void_p), ("col_idx", C.c_void_p), ("values", C.c_void_p)]
+
+
+class mcmi_stats(C.Structure):
+    _fields_ = [
+        ("n_chains", C.c_int64),
+        ("max_len", C.c_int64),
+        ("a_norm", C.c_double),
+        ("rows", C.c_int64),
+        ("nnz", C.c_int64),
+        ("walk_steps", C.c_int64),
+        ("walk_deg_sum", C.c_int64),
+        ("hash_cap", C.c_int64),
+        ("rows_retried", C.c_int64),
+        ("ms_tables", C.c_double),
+        ("ms_walk", C.c_double),
+        ("ms_assemble", C.c_double),
+        ("ms_total", C.c_double),
+        ("launches", C.c_int64),
+        ("ms_walk_kernel", C.c_double),
+    ]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+class mcmi_device_csr(C.Structure):
+    _fields_ = [
+        ("row_begin", C.c_int64),
+        ("row_end", C.c_int64),
+        ("nnz", C.c_int64),
+        ("row_ptr", C.c_void_p),
+        ("col_idx", C.c_void_p),
+        ("values", C.c_void_p),
+        ("chains_used", C.c_void_p),
+        ("entries_before", C.c_void_p),
+    ]
+
+
+_lib = None
+
+
+def load(path: str | None = None):
+    """Loads libmcmi.so; raises if it has not been built (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    path = path or LIB
+    if not os.path.exists(path):
+        raise ImportError(
+            f"{path} not found: the CUDA library is required (run `python -m paper_2409_03095_b200.build`)")
+    L = C.CDLL(path)
+    L.mcmi_config_default.argtypes = [C.POINTER(mcmi_config)]
+    L.mcmi_config_default.restype = None
+    L.mcmi_build.argtypes = [C.POINTER(mcmi_csr_view), C.POINTER(mcmi_config), C.POINTER(C.c_void_p),
+                             C.c_char_p, C.c_size_t]
+    L.mcmi_build_rows.argtypes = [C.POINTER(mcmi_csr_view), C.POINTER(mcmi_config), C.c_int64, C.c_int64,
+                                  C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+    L.mcmi_result_sizes.argtypes = [C.c_void_p, _i64p, _i64p]
+    L.mcmi_result_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                   _i64p, _i64p]
+    L.mcmi_result_stats.argtypes = [C.c_void_p, C.POINTER(mcmi_stats)]
+    L.mcmi_result_free.argtypes = [C.c_void_p]
+    L.mcmi_result_free.restype = None
+    L.mcmi_engine_create.argtypes = [C.c_int, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+    L.mcmi_engine_destroy.argtypes = [C.c_void_p]
+    L.mcmi_engine_destroy.restype = None
+    L.mcmi_engine_build.argtypes = [C.c_void_p, C.POINTER(mcmi_csr_view), C.POINTER(mcmi_config), C.c_int64,
+                                    C.c_int64, C.c_void_p, C.POINTER(mcmi_device_csr), C.POINTER(mcmi_stats),
+                                    C.c_char_p, C.c_size_t]
+    L.mcmi_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
+    L.mcmi_version.restype = C.c_char_p
+    _lib = L
+    return L

@@ -1,0 +1,665 @@
+// engine.cu — host orchestration of the device pipeline and the C-ABI
+// (include/mcmi.h).  Mirrors run_pipeline (mc_engine.cpp:153-226):
+//   drop -> augment/split -> transition tables      (tables.cu, device)
+//   derive_chain_budget                             (host, glibc log/ceil)
+//   walk + accumulate + finalize per row            (walk.cu, device)
+//   CSR assembly in row order                       (assemble.cu, device)
+// There is no CPU fallback: every failure to reach the device is an error.
+#include <algorithm>
+#include <climits>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/mcmi.h"
+#include "kernels.cuh"
+
+using namespace mcmi;
+
+namespace {
+
+struct Status {
+    int code = MCMI_OK;
+    std::string msg;
+};
+
+Status ok() { return {}; }
+Status fail(int code, std::string msg) { return {code, std::move(msg)}; }
+
+Status cuda_status(cudaError_t e, const char* what) {
+    if (e == cudaSuccess) return ok();
+    cudaGetLastError();  // clear sticky non-fatal errors
+    const int code = (e == cudaErrorMemoryAllocation) ? MCMI_ENOMEM
+                     : (e == cudaErrorNoDevice || e == cudaErrorInvalidDevice ||
+                        e == cudaErrorInsufficientDriver)
+                         ? MCMI_ENODEV
+                         : MCMI_ECUDA;
+    return fail(code, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define MCMI_TRY(expr, what)                                   \
+    do {                                                       \
+        Status st__ = cuda_status((expr), (what));             \
+        if (st__.code) return st__;                            \
+    } while (0)
+
+int report(const Status& st, char* err, size_t errlen) {
+    if (err && errlen) {
+        std::strncpy(err, st.msg.c_str(), errlen - 1);
+        err[errlen - 1] = 0;
+    }
+    return st.code;
+}
+
+// Grow-only device buffer.
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+    cudaError_t ensure(size_t bytes) {
+        if (bytes == 0) bytes = 1;
+        if (bytes <= cap) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        const size_t want = bytes + bytes / 8;
+        cudaError_t e = cudaMalloc(&p, want);
+        if (e != cudaSuccess) return e;
+        cap = want;
+        return cudaSuccess;
+    }
+    // Grow keeping the first `keep` bytes (stream-ordered copy).
+    cudaError_t grow_preserve(size_t bytes, size_t keep, cudaStream_t s) {
+        if (bytes <= cap) return cudaSuccess;
+        void* q = nullptr;
+        const size_t want = bytes + bytes / 4;
+        cudaError_t e = cudaMalloc(&q, want);
+        if (e != cudaSuccess) return e;
+        if (p && keep) {
+            e = cudaMemcpyAsync(q, p, keep, cudaMemcpyDeviceToDevice, s);
+            if (e != cudaSuccess) return e;
+            e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) return e;
+        }
+        if (p) cudaFree(p);
+        p = q;
+        cap = want;
+        return cudaSuccess;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    template <class T>
+    T* as() const {
+        return static_cast<T*>(p);
+    }
+};
+
+int64_t next_pow2(int64_t x) {
+    int64_t p = 1;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+int64_t sat_mul(int64_t a, int64_t b) {
+    if (a <= 0 || b <= 0) return 0;
+    if (a > INT64_MAX / b) return INT64_MAX;
+    return a * b;
+}
+
+// derive_chain_budget (mc_engine.cpp:12-33), on the host so glibc's log and
+// ceil give the reference's exact (N, L).
+Status chain_budget(const mcmi_config& c, double a_norm, int64_t* nc, int64_t* ml) {
+    if (!(a_norm >= 0.0 && a_norm < 1.0)) return fail(MCMI_EINVAL, "||A|| must lie in [0,1)");
+    int64_t n_chains, max_len;
+    if (c.has_chains_override) {
+        n_chains = c.chains_override;
+    } else {
+        const double root = 0.6745 / (c.epsilon * (1.0 - a_norm));
+        const double sq = std::ceil(root * root);
+        if (!(sq < 9.2e18)) return fail(MCMI_EINVAL, "chain budget overflows int64 (epsilon too small)");
+        n_chains = static_cast<int64_t>(sq);
+    }
+    if (c.has_max_len_override) {
+        max_len = c.max_len_override;
+    } else if (a_norm <= 0.0) {
+        max_len = 1;
+    } else {
+        const double len = std::log(c.delta) / std::log(a_norm);
+        const double cl = std::ceil(len);
+        max_len = cl < 9.2e18 ? std::max<int64_t>(1, static_cast<int64_t>(cl)) : INT64_MAX;
+    }
+    n_chains = std::max<int64_t>(1, n_chains);
+    *nc = n_chains;
+    *ml = max_len;
+    return ok();
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- engine
+
+struct mcmi_engine {
+    int device = 0;
+    int num_sms = 148;
+    cudaStream_t own = nullptr;
+    cudaEvent_t ev[6] = {};
+    DevBuf red, diag_val, a_cnt, a_off, keep, desc, ent, colA, b1, scan_tmp, cq_tmp;
+    DevBuf stage_col, stage_val, row_cnt, row_src, chains_used, entries_before, counters;
+    DevBuf ovf[2];
+    DevBuf out_rp, out_col, out_val;
+    Reductions* h_red = nullptr;          // pinned
+    unsigned long long* h_ctr = nullptr;  // pinned [8]
+    int64_t* h_i64 = nullptr;             // pinned [4]
+    mcmi_device_csr last{};
+};
+
+namespace {
+
+Status engine_init(mcmi_engine* e, int device) {
+    int count = 0;
+    MCMI_TRY(cudaGetDeviceCount(&count), "cudaGetDeviceCount");
+    if (device < 0 || device >= count)
+        return fail(MCMI_ENODEV, "CUDA device " + std::to_string(device) + " not present (" +
+                                     std::to_string(count) + " visible)");
+    e->device = device;
+    MCMI_TRY(cudaSetDevice(device), "cudaSetDevice");
+    cudaDeviceProp prop{};
+    MCMI_TRY(cudaGetDeviceProperties(&prop, device), "cudaGetDeviceProperties");
+    if (prop.major < 10)
+        return fail(MCMI_ENODEV, std::string("device ") + prop.name + " is not sm_100 (Blackwell)");
+    e->num_sms = prop.multiProcessorCount;
+    MCMI_TRY(cudaStreamCreateWithFlags(&e->own, cudaStreamNonBlocking), "cudaStreamCreate");
+    for (auto& ev : e->ev) MCMI_TRY(cudaEventCreate(&ev), "cudaEventCreate");
+    MCMI_TRY(cudaMallocHost(&e->h_red, sizeof(Reductions)), "cudaMallocHost");
+    MCMI_TRY(cudaMallocHost(&e->h_ctr, 8 * sizeof(unsigned long long)), "cudaMallocHost");
+    MCMI_TRY(cudaMallocHost(&e->h_i64, 4 * sizeof(int64_t)), "cudaMallocHost");
+    return ok();
+}
+
+void engine_release(mcmi_engine* e) {
+    cudaSetDevice(e->device);
+    for (DevBuf* b : {&e->red, &e->diag_val, &e->a_cnt, &e->a_off, &e->keep, &e->desc, &e->ent,
+                      &e->colA, &e->b1, &e->scan_tmp, &e->cq_tmp, &e->stage_col, &e->stage_val,
+                      &e->row_cnt, &e->row_src, &e->chains_used, &e->entries_before,
+                      &e->counters, &e->ovf[0], &e->ovf[1], &e->out_rp, &e->out_col,
+                      &e->out_val})
+        b->release();
+    for (auto& ev : e->ev)
+        if (ev) cudaEventDestroy(ev);
+    if (e->own) cudaStreamDestroy(e->own);
+    if (e->h_red) cudaFreeHost(e->h_red);
+    if (e->h_ctr) cudaFreeHost(e->h_ctr);
+    if (e->h_i64) cudaFreeHost(e->h_i64);
+}
+
+constexpr int kLogMax = 256;  // deposit-log entries per warp (shared memory)
+
+struct Tier {
+    int cap, cap_limit, lanes, log_stride, warps_per_block;
+};
+
+Tier make_tier(int cap, int64_t max_len) {
+    Tier t;
+    t.cap = cap;
+    t.cap_limit = cap - cap / 4;
+    const int64_t s64 = std::max<int64_t>(1, max_len) + 1;
+    t.log_stride = static_cast<int>(std::min<int64_t>(s64, INT_MAX / 64));
+    const int logmax = std::max(kLogMax, t.log_stride);
+    t.lanes = std::max(1, std::min(32, logmax / t.log_stride));
+    const size_t per_warp = walk_smem_bytes_per_warp(t.cap, t.lanes, t.log_stride);
+    t.warps_per_block = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, (96u * 1024u) / per_warp)));
+    return t;
+}
+
+// The full build of rows [row_begin, row_end) from device CSR `b`.
+Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& cfg,
+                    int64_t row_begin, int64_t row_end, cudaStream_t s, mcmi_device_csr* out,
+                    mcmi_stats* stats) {
+    const int64_t n = b.n;
+    mcmi_stats st{};
+    if (n < 0) return fail(MCMI_EINVAL, "negative dimension");
+    if (n > INT_MAX - 1) return fail(MCMI_EINVAL, "dimension exceeds 2^31-2 rows");
+    if (row_begin < 0) row_begin = 0;
+    if (row_end < 0 || row_end > n) row_end = n;
+    if (row_end < row_begin) row_end = row_begin;
+    const int64_t rows = row_end - row_begin;
+    // csr.cpp:128-129 comes first in the reference pipeline, then split.cpp:48
+    if (!(cfg.drop_fraction >= 0.0 && cfg.drop_fraction <= 1.0))
+        return fail(MCMI_EINVAL, "drop fraction must lie in [0,1]");
+    if (!(cfg.alpha > 0.0)) return fail(MCMI_EINVAL, "alpha must be positive");
+    if (cfg.rng_mode != MCMI_RNG_REFERENCE && cfg.rng_mode != MCMI_RNG_KEYED)
+        return fail(MCMI_EINVAL, "rng_mode must be MCMI_RNG_REFERENCE or MCMI_RNG_KEYED");
+    MCMI_TRY(cudaSetDevice(e->device), "cudaSetDevice");
+
+    MCMI_TRY(cudaEventRecord(e->ev[0], s), "cudaEventRecord");
+    int64_t nnz = 0;
+    if (n > 0) {
+        MCMI_TRY(cudaMemcpyAsync(e->h_i64, b.row_ptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s),
+                 "read row_ptr[n]");
+        MCMI_TRY(cudaStreamSynchronize(s), "cudaStreamSynchronize");
+        nnz = e->h_i64[0];
+        if (nnz < 0) return fail(MCMI_EINVAL, "row_ptr[n] is negative");
+    }
+    const int64_t n1 = std::max<int64_t>(n, 1);
+    const int64_t z1 = std::max<int64_t>(nnz, 1);
+
+    // ---- subsystem 1: tables
+    MCMI_TRY(e->red.ensure(sizeof(Reductions)), "alloc");
+    MCMI_TRY(e->diag_val.ensure(n1 * sizeof(double)), "alloc diag");
+    MCMI_TRY(e->a_cnt.ensure(n1 * sizeof(unsigned)), "alloc a_cnt");
+    MCMI_TRY(e->a_off.ensure((n1 + 1) * sizeof(unsigned)), "alloc a_off");
+    MCMI_TRY(e->desc.ensure(n1 * sizeof(uint2)), "alloc desc");
+    MCMI_TRY(e->ent.ensure(z1 * sizeof(double2)), "alloc ent");
+    MCMI_TRY(e->colA.ensure(z1 * sizeof(int)), "alloc col");
+    MCMI_TRY(e->b1.ensure(n1 * sizeof(double)), "alloc b1");
+    MCMI_TRY(e->scan_tmp.ensure(scan_scratch_bytes(std::max(n1, z1)) + 64), "alloc scan");
+
+    Reductions init{};
+    init.offmin_bits = 0x7ff0000000000000ull;
+    init.degenerate_row = LLONG_MAX;
+    init.bad_col_row = LLONG_MAX;
+    *e->h_red = init;
+    MCMI_TRY(cudaMemcpyAsync(e->red.p, e->h_red, sizeof(Reductions), cudaMemcpyHostToDevice, s),
+             "init reductions");
+
+    TableBuildArgs ta{};
+    ta.n = n;
+    ta.row_ptr = b.row_ptr;
+    ta.col_idx = b.col_idx;
+    ta.values = b.values;
+    ta.drop_fraction = cfg.drop_fraction;
+    ta.drop_mode = cfg.drop_mode;
+    ta.alpha = cfg.alpha;
+    ta.mode = cfg.mode == MCMI_AUGMENT_PLAIN ? 0 : 1;
+    ta.red = e->red.as<Reductions>();
+    ta.diag_val = e->diag_val.as<double>();
+    ta.a_cnt = e->a_cnt.as<unsigned>();
+    ta.a_off = e->a_off.as<unsigned>();
+    ta.keep = nullptr;
+    ta.desc = e->desc.as<uint2>();
+    ta.ent = e->ent.as<double2>();
+    ta.col = e->colA.as<int>();
+    ta.b1_diag = e->b1.as<double>();
+    const bool drop_active = cfg.drop_fraction != 0.0 && n > 0;
+    const int64_t scan_launches_n = (n > 0 ? 3 : 1);
+    if (drop_active && cfg.drop_mode == MCMI_DROP_COUNT_QUANTILE) {
+        MCMI_TRY(e->keep.ensure(z1), "alloc keep");
+        MCMI_TRY(e->cq_tmp.ensure(count_quantile_scratch_bytes(z1)), "alloc cq");
+        ta.keep = e->keep.as<unsigned char>();
+        MCMI_TRY(launch_count_quantile(ta, nnz, 0, e->cq_tmp.p, e->cq_tmp.cap, s), "count-quantile drop");
+        st.launches += 2 + 2 * 8 + 1 + (nnz > 0 ? 3 : 1) + 1;
+    }
+    if (n > 0) {
+        MCMI_TRY(launch_table_build(ta, nnz, drop_active, s), "table build");
+        MCMI_TRY(scan_u32_exclusive(ta.a_cnt, ta.a_off, n, e->scan_tmp.p, s), "scan a_cnt");
+        MCMI_TRY(launch_table_fill(ta, s), "table fill");
+        st.launches += (drop_active && cfg.drop_mode == MCMI_DROP_VALUE_RANGE ? 3 : 2) + scan_launches_n + 1;
+    }
+    MCMI_TRY(cudaMemcpyAsync(e->h_red, e->red.p, sizeof(Reductions), cudaMemcpyDeviceToHost, s),
+             "read reductions");
+    MCMI_TRY(cudaEventRecord(e->ev[1], s), "cudaEventRecord");
+    MCMI_TRY(cudaStreamSynchronize(s), "table build");
+    const Reductions red = *e->h_red;
+    if (red.bad_col_row != LLONG_MAX)
+        return fail(MCMI_ERANGE, "column index out of range in row " + std::to_string(red.bad_col_row));
+    if (red.degenerate_row != LLONG_MAX)  // split.cpp:67-69
+        return fail(MCMI_ESPLIT, "degenerate diagonal after augmentation at row " +
+                                     std::to_string(red.degenerate_row));
+    double a_norm;
+    std::memcpy(&a_norm, &red.anorm_bits, sizeof(double));
+    if (!(a_norm < 1.0))  // split.cpp:94-96
+        return fail(MCMI_ESPLIT, "diagonal dominance failure: ||A||inf = " + std::to_string(a_norm));
+    if (red.a_nnz >= (1ull << 32)) return fail(MCMI_EINVAL, "A has 2^32 or more entries");
+    int64_t N = 1, L = 1;
+    Status bs = chain_budget(cfg, a_norm, &N, &L);
+    if (bs.code) return bs;
+    st.n_chains = N;
+    st.max_len = L;
+    st.a_norm = a_norm;
+    st.rows = rows;
+
+    // ---- subsystems 2 + 3: walks, accumulate, finalize
+    const int64_t dmax = static_cast<int64_t>(red.max_deg);
+    int64_t reach = 1, term = 1;  // 1 + d + d^2 + ... + d^L (saturating)
+    for (int64_t t = 0; t < std::max<int64_t>(L, 0) && reach < (1 << 20); ++t) {
+        term = sat_mul(term, dmax);
+        if (term == 0) break;
+        reach = (reach > INT64_MAX - term) ? INT64_MAX : reach + term;
+    }
+    const int64_t deposits = sat_mul(N, std::max<int64_t>(L, 0));  // distinct <= 1 + N*L
+    int64_t bound = std::min<int64_t>(n1, reach);
+    if (deposits < INT64_MAX) bound = std::min<int64_t>(bound, deposits + 1);
+    static const int kTierCaps[] = {256, 1024, 4096};
+    int first_cap = static_cast<int>(std::min<int64_t>(256, std::max<int64_t>(32, next_pow2((bound * 4 + 2) / 3))));
+    std::vector<Tier> tiers;
+    tiers.push_back(make_tier(first_cap, L));
+    for (int c : kTierCaps)
+        if (c > first_cap && (tiers.back().cap_limit < bound)) tiers.push_back(make_tier(c, L));
+    st.hash_cap = first_cap;
+
+    MCMI_TRY(e->row_cnt.ensure(std::max<int64_t>(rows, 1) * sizeof(int)), "alloc row_cnt");
+    MCMI_TRY(e->row_src.ensure(std::max<int64_t>(rows, 1) * sizeof(int64_t)), "alloc row_src");
+    MCMI_TRY(e->chains_used.ensure(std::max<int64_t>(rows, 1) * sizeof(int64_t)), "alloc meta");
+    MCMI_TRY(e->entries_before.ensure(std::max<int64_t>(rows, 1) * sizeof(int64_t)), "alloc meta");
+    MCMI_TRY(e->counters.ensure(8 * sizeof(unsigned long long)), "alloc counters");
+    MCMI_TRY(e->ovf[0].ensure(std::max<int64_t>(rows, 1) * sizeof(int)), "alloc overflow");
+    MCMI_TRY(e->ovf[1].ensure(std::max<int64_t>(rows, 1) * sizeof(int)), "alloc overflow");
+
+    auto stride_of = [&](const Tier& t) -> int64_t {
+        int64_t sst = std::min<int64_t>(t.cap_limit, bound);
+        if (cfg.retain_k > 0) sst = std::min<int64_t>(sst, cfg.retain_k);
+        return std::max<int64_t>(sst, 1);
+    };
+    int64_t pool_used = 0;
+    int64_t work = rows;
+    const int* row_list = nullptr;
+    int cur = 0;
+    unsigned long long total_steps = 0, total_deg = 0;
+    for (size_t ti = 0; ti < tiers.size() && work > 0; ++ti) {
+        const Tier& t = tiers[ti];
+        const int64_t stride = stride_of(t);
+        const int64_t need = pool_used + work * stride;
+        MCMI_TRY(e->stage_col.grow_preserve(need * sizeof(int), pool_used * sizeof(int), s), "alloc staging");
+        MCMI_TRY(e->stage_val.grow_preserve(need * sizeof(double), pool_used * sizeof(double), s),
+                 "alloc staging");
+        MCMI_TRY(cudaMemsetAsync(e->counters.p, 0, 8 * sizeof(unsigned long long), s), "memset");
+        WalkArgs wa{};
+        wa.t = Tables{n, e->desc.as<uint2>(), e->ent.as<double2>(), e->colA.as<int>(), e->b1.as<double>()};
+        wa.row_begin = row_begin;
+        wa.row_list = row_list;
+        wa.n_work = work;
+        wa.n_chains = N;
+        wa.max_len = L;
+        wa.delta = cfg.delta;
+        wa.seed = cfg.master_seed;
+        wa.retain_k = cfg.retain_k;
+        wa.rng_mode = cfg.rng_mode;
+        wa.cap = t.cap;
+        wa.cap_limit = t.cap_limit;
+        wa.lanes = t.lanes;
+        wa.log_stride = t.log_stride;
+        wa.ell0 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(L, 2)));
+        wa.stage_col = e->stage_col.as<int>();
+        wa.stage_val = e->stage_val.as<double>();
+        wa.stage_base = pool_used;
+        wa.stage_stride = stride;
+        wa.row_cnt = e->row_cnt.as<int>();
+        wa.row_src = e->row_src.as<int64_t>();
+        wa.chains_used = e->chains_used.as<int64_t>();
+        wa.entries_before = e->entries_before.as<int64_t>();
+        wa.counters = e->counters.as<unsigned long long>();
+        wa.overflow_list = e->ovf[cur].as<int>();
+        MCMI_TRY(cudaEventRecord(e->ev[4], s), "cudaEventRecord");
+        MCMI_TRY(launch_walk(wa, t.warps_per_block, e->num_sms, s), "walk kernel");
+        MCMI_TRY(cudaEventRecord(e->ev[5], s), "cudaEventRecord");
+        st.launches += 1;
+        MCMI_TRY(cudaMemcpyAsync(e->h_ctr, e->counters.p, 8 * sizeof(unsigned long long),
+                                 cudaMemcpyDeviceToHost, s),
+                 "read counters");
+        MCMI_TRY(cudaStreamSynchronize(s), "walk kernel");
+        float tw = 0;
+        cudaEventElapsedTime(&tw, e->ev[4], e->ev[5]);
+        st.ms_walk_kernel += tw;
+        total_steps += e->h_ctr[1];
+        total_deg += e->h_ctr[2];
+        pool_used += work * stride;
+        const int64_t overflowed = static_cast<int64_t>(e->h_ctr[3]);
+        if (ti > 0) st.rows_retried += work;
+        work = overflowed;
+        row_list = e->ovf[cur].as<int>();
+        cur ^= 1;
+    }
+    if (work > 0)
+        return fail(MCMI_ENOMEM, std::to_string(work) +
+                                     " rows touch more than 3072 distinct columns; the "
+                                     "accumulator tier for such rows is not available");
+    st.walk_steps = static_cast<int64_t>(total_steps);
+    st.walk_deg_sum = static_cast<int64_t>(total_deg);
+    MCMI_TRY(cudaEventRecord(e->ev[2], s), "cudaEventRecord");
+
+    // ---- assembly (mc_engine.cpp:207-225)
+    MCMI_TRY(e->out_rp.ensure((rows + 1) * sizeof(int64_t)), "alloc row_ptr");
+    MCMI_TRY(scan_rows_exclusive(e->row_cnt.as<int>(), e->out_rp.as<int64_t>(), rows, e->scan_tmp.p, s),
+             "scan rows");
+    MCMI_TRY(cudaMemcpyAsync(e->h_i64, e->out_rp.as<int64_t>() + rows, sizeof(int64_t),
+                             cudaMemcpyDeviceToHost, s),
+             "read nnz");
+    MCMI_TRY(cudaStreamSynchronize(s), "scan rows");
+    const int64_t out_nnz = e->h_i64[0];
+    MCMI_TRY(e->out_col.ensure(std::max<int64_t>(out_nnz, 1) * sizeof(int64_t)), "alloc col");
+    MCMI_TRY(e->out_val.ensure(std::max<int64_t>(out_nnz, 1) * sizeof(double)), "alloc val");
+    MCMI_TRY(launch_compact(e->stage_col.as<int>(), e->stage_val.as<double>(), e->row_src.as<int64_t>(),
+                            e->row_cnt.as<int>(), e->out_rp.as<int64_t>(), rows, e->out_col.as<int64_t>(),
+                            e->out_val.as<double>(), s),
+             "compact");
+    st.launches += (rows > 0 ? 3 : 1) + (rows > 0 ? 1 : 0);
+    MCMI_TRY(cudaEventRecord(e->ev[3], s), "cudaEventRecord");
+    MCMI_TRY(cudaStreamSynchronize(s), "assembly");
+    float t01 = 0, t12 = 0, t23 = 0, t03 = 0;
+    cudaEventElapsedTime(&t01, e->ev[0], e->ev[1]);
+    cudaEventElapsedTime(&t12, e->ev[1], e->ev[2]);
+    cudaEventElapsedTime(&t23, e->ev[2], e->ev[3]);
+    cudaEventElapsedTime(&t03, e->ev[0], e->ev[3]);
+    st.ms_tables = t01;
+    st.ms_walk = t12;
+    st.ms_assemble = t23;
+    st.ms_total = t03;
+    st.nnz = out_nnz;
+
+    out->row_begin = row_begin;
+    out->row_end = row_end;
+    out->nnz = out_nnz;
+    out->row_ptr = e->out_rp.as<int64_t>();
+    out->col_idx = e->out_col.as<int64_t>();
+    out->values = e->out_val.as<double>();
+    out->chains_used = e->chains_used.as<int64_t>();
+    out->entries_before = e->entries_before.as<int64_t>();
+    e->last = *out;
+    if (stats) *stats = st;
+    return ok();
+}
+
+// One cached engine per device for the host API (buffers reused across calls).
+std::mutex g_cache_mu;
+std::vector<mcmi_engine*> g_cache;  // idle engines
+
+mcmi_engine* acquire_engine(int device, Status* st) {
+    {
+        std::lock_guard<std::mutex> lk(g_cache_mu);
+        for (size_t i = 0; i < g_cache.size(); ++i)
+            if (g_cache[i]->device == device) {
+                mcmi_engine* e = g_cache[i];
+                g_cache.erase(g_cache.begin() + static_cast<long>(i));
+                return e;
+            }
+    }
+    auto* e = new mcmi_engine();
+    *st = engine_init(e, device);
+    if (st->code) {
+        engine_release(e);
+        delete e;
+        return nullptr;
+    }
+    return e;
+}
+
+void release_engine(mcmi_engine* e) {
+    std::lock_guard<std::mutex> lk(g_cache_mu);
+    g_cache.push_back(e);
+}
+
+}  // namespace
+
+struct mcmi_result {
+    int device = 0;
+    int64_t n = 0, nnz = 0;
+    int64_t n_chains = 1, max_len = 1;
+    mcmi_stats stats{};
+    // device arrays owned by the result
+    int64_t* rp = nullptr;
+    int64_t* ci = nullptr;
+    double* v = nullptr;
+    int64_t* cu = nullptr;
+    int64_t* eb = nullptr;
+};
+
+extern "C" {
+
+void mcmi_config_default(mcmi_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->epsilon = 0.0625;
+    c->delta = 0.0625;
+    c->alpha = 5.0;
+    c->mode = MCMI_AUGMENT_SIGN_AWARE;
+    c->drop_mode = MCMI_DROP_VALUE_RANGE;
+    c->rng_mode = MCMI_RNG_REFERENCE;
+}
+
+const char* mcmi_version(void) { return "mcmi 1 sm_100a"; }
+
+int mcmi_engine_create(int device, mcmi_engine** out, char* err, size_t errlen) {
+    *out = nullptr;
+    auto* e = new mcmi_engine();
+    Status st = engine_init(e, device);
+    if (st.code) {
+        engine_release(e);
+        delete e;
+        return report(st, err, errlen);
+    }
+    *out = e;
+    return MCMI_OK;
+}
+
+void mcmi_engine_destroy(mcmi_engine* e) {
+    if (!e) return;
+    engine_release(e);
+    delete e;
+}
+
+int mcmi_engine_build(mcmi_engine* e, const mcmi_csr_view* b, const mcmi_config* cfg,
+                      int64_t row_begin, int64_t row_end, void* stream, mcmi_device_csr* out,
+                      mcmi_stats* stats, char* err, size_t errlen) {
+    if (!e || !b || !cfg || !out) return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e->own;
+    return report(engine_build(e, *b, *cfg, row_begin, row_end, s, out, stats), err, errlen);
+}
+
+int mcmi_build(const mcmi_csr_view* b, const mcmi_config* cfg, mcmi_result** out, char* err,
+               size_t errlen) {
+    return mcmi_build_rows(b, cfg, 0, -1, out, err, errlen);
+}
+
+int mcmi_build_rows(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_begin,
+                    int64_t row_end, mcmi_result** out, char* err, size_t errlen) {
+    *out = nullptr;
+    if (!b || !cfg) return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    Status st;
+    mcmi_engine* e = acquire_engine(cfg->device, &st);
+    if (!e) return report(st, err, errlen);
+    auto run = [&]() -> Status {
+        const int64_t n = b->n;
+        if (n < 0) return fail(MCMI_EINVAL, "negative dimension");
+        const int64_t nnz = n > 0 ? b->row_ptr[n] : 0;
+        cudaStream_t s = e->own;
+        // input staging: reuse engine-owned device buffers (grow-only)
+        void *d_rp = nullptr, *d_ci = nullptr, *d_v = nullptr;
+        MCMI_TRY(cudaMallocAsync(&d_rp, (std::max<int64_t>(n, 0) + 1) * sizeof(int64_t), s), "alloc B");
+        MCMI_TRY(cudaMallocAsync(&d_ci, std::max<int64_t>(nnz, 1) * sizeof(int64_t), s), "alloc B");
+        MCMI_TRY(cudaMallocAsync(&d_v, std::max<int64_t>(nnz, 1) * sizeof(double), s), "alloc B");
+        MCMI_TRY(cudaMemcpyAsync(d_rp, b->row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDefault, s), "H2D");
+        if (nnz > 0) {
+            MCMI_TRY(cudaMemcpyAsync(d_ci, b->col_idx, nnz * sizeof(int64_t), cudaMemcpyDefault, s), "H2D");
+            MCMI_TRY(cudaMemcpyAsync(d_v, b->values, nnz * sizeof(double), cudaMemcpyDefault, s), "H2D");
+        }
+        mcmi_csr_view dv{n, static_cast<int64_t*>(d_rp), static_cast<int64_t*>(d_ci),
+                         static_cast<double*>(d_v)};
+        mcmi_device_csr dc{};
+        mcmi_stats stats{};
+        Status bst = engine_build(e, dv, *cfg, row_begin, row_end, s, &dc, &stats);
+        cudaFreeAsync(d_rp, s);
+        cudaFreeAsync(d_ci, s);
+        cudaFreeAsync(d_v, s);
+        if (bst.code) return bst;
+        auto* r = new mcmi_result();
+        r->device = e->device;
+        r->n = dc.row_end - dc.row_begin;
+        r->nnz = dc.nnz;
+        r->n_chains = stats.n_chains;
+        r->max_len = stats.max_len;
+        r->stats = stats;
+        // hand the engine's output buffers to the result (no device copy)
+        r->rp = dc.row_ptr;
+        r->ci = dc.col_idx;
+        r->v = dc.values;
+        r->cu = dc.chains_used;
+        r->eb = dc.entries_before;
+        e->out_rp = DevBuf{};
+        e->out_col = DevBuf{};
+        e->out_val = DevBuf{};
+        e->chains_used = DevBuf{};
+        e->entries_before = DevBuf{};
+        *out = r;
+        return ok();
+    };
+    st = run();
+    release_engine(e);
+    return report(st, err, errlen);
+}
+
+int mcmi_result_sizes(const mcmi_result* r, int64_t* n, int64_t* nnz) {
+    if (!r) return MCMI_EINVAL;
+    if (n) *n = r->n;
+    if (nnz) *nnz = r->nnz;
+    return MCMI_OK;
+}
+
+int mcmi_result_copy(const mcmi_result* r, int64_t* row_ptr, int64_t* col_idx, double* values,
+                     int64_t* chains_used, int64_t* entries_before, int64_t* n_chains,
+                     int64_t* max_len) {
+    if (!r) return MCMI_EINVAL;
+    if (cudaSetDevice(r->device) != cudaSuccess) return MCMI_ECUDA;
+    cudaError_t e = cudaSuccess;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+        if (dst && src && bytes && e == cudaSuccess) e = cudaMemcpy(dst, src, bytes, cudaMemcpyDefault);
+    };
+    cp(row_ptr, r->rp, (r->n + 1) * sizeof(int64_t));
+    cp(col_idx, r->ci, r->nnz * sizeof(int64_t));
+    cp(values, r->v, r->nnz * sizeof(double));
+    cp(chains_used, r->cu, r->n * sizeof(int64_t));
+    cp(entries_before, r->eb, r->n * sizeof(int64_t));
+    if (n_chains) *n_chains = r->n_chains;
+    if (max_len) *max_len = r->max_len;
+    return e == cudaSuccess ? MCMI_OK : MCMI_ECUDA;
+}
+
+int mcmi_result_stats(const mcmi_result* r, mcmi_stats* stats) {
+    if (!r || !stats) return MCMI_EINVAL;
+    *stats = r->stats;
+    return MCMI_OK;
+}
+
+void mcmi_result_free(mcmi_result* r) {
+    if (!r) return;
+    cudaSetDevice(r->device);
+    cudaFree(r->rp);
+    cudaFree(r->ci);
+    cudaFree(r->v);
+    cudaFree(r->cu);
+    cudaFree(r->eb);
+    delete r;
+}
+
+int mcmi_copy(void* dst, const void* src, size_t bytes, void* stream) {
+    const cudaError_t e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault,
+                                          static_cast<cudaStream_t>(stream));
+    return e == cudaSuccess ? MCMI_OK : MCMI_ECUDA;
+}
+
+}  // extern "C"

@@ -1,0 +1,106 @@
+// kernels.cuh — internal interface between the host engine and the kernels.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mcmi {
+
+// Device-side scalar reductions and error slots of one build (zeroed per build).
+struct Reductions {
+    unsigned long long offmin_bits;  // min |b_ij| over off-diagonals (csr.cpp:88-105)
+    unsigned long long offmax_bits;  // max |b_ij| over off-diagonals
+    unsigned long long bnorm_bits;   // ||B_reduced||inf (csr.cpp:77-86)
+    unsigned long long anorm_bits;   // ||A||inf (split.cpp:83-92)
+    long long degenerate_row;        // first row with b_hat_ii == 0 (split.cpp:67-69), else LLONG_MAX
+    long long bad_col_row;           // first row holding a column outside [0,n), else LLONG_MAX
+    unsigned long long max_deg;      // max row length of A
+    unsigned long long a_nnz;        // entries of A
+    unsigned long long cq_threshold_bits;  // count-quantile: |v| of the n_drop-th smallest
+    long long cq_tie_budget;               // count-quantile: ties at the threshold to drop
+    unsigned long long pad[6];
+};
+
+// Transition tables (subsystem 1), one record per state s of the walk:
+//   desc[s] = {begin, deg} into the entry arrays (A's row s)
+//   ent[k]  = {cum_k, ratio_k}: running sequential sum of p (sample_transition's
+//             `cum`, mc_engine.cpp:71-75) and a_k / p_k (mc_engine.cpp:94)
+//   col[k]  = column of A (int32)
+struct Tables {
+    int64_t n;
+    const uint2* desc;
+    const double2* ent;
+    const int* col;
+    const double* b1_diag;  // diag(B_hat) = B1 (split.cpp:70)
+};
+
+struct TableBuildArgs {
+    int64_t n;
+    const int64_t* row_ptr;
+    const int64_t* col_idx;
+    const double* values;
+    double drop_fraction;
+    int drop_mode;
+    double alpha;
+    int mode;
+    // scratch / outputs
+    Reductions* red;
+    double* diag_val;     // [n]
+    unsigned* a_cnt;      // [n]
+    unsigned* a_off;      // [n+1]
+    unsigned char* keep;  // [nnz] count-quantile keep flags (or nullptr)
+    uint2* desc;
+    double2* ent;
+    int* col;
+    double* b1_diag;
+};
+
+// Walk + accumulate + per-row finalize (subsystems 2 and 3).
+struct WalkArgs {
+    Tables t;
+    int64_t row_begin;      // global index of local row 0
+    const int* row_list;    // nullptr: work item i is row row_begin + i
+    int64_t n_work;
+    int64_t n_chains, max_len;
+    double delta;
+    uint64_t seed;
+    int64_t retain_k;
+    int rng_mode;
+    int cap;                // hash capacity (power of two)
+    int cap_limit;          // max distinct columns before the row overflows to the next tier
+    int lanes;              // chains per batch (<= 32)
+    int log_stride;         // max_len + 1 deposits per chain
+    int ell0;               // initial speculative draw stride (reference-stream mode)
+    // outputs, indexed by local row (row - row_begin)
+    int* stage_col;
+    double* stage_val;
+    int64_t stage_base;     // offset of work item 0 in the staging pool
+    int64_t stage_stride;   // entries per work item
+    int* row_cnt;
+    int64_t* row_src;
+    int64_t* chains_used;
+    int64_t* entries_before;
+    unsigned long long* counters;  // [0] work cursor [1] steps [2] deg_sum [3] overflow count
+    int* overflow_list;
+};
+
+cudaError_t launch_table_build(const TableBuildArgs& a, int64_t nnz, bool drop_active,
+                               cudaStream_t s);
+cudaError_t launch_table_fill(const TableBuildArgs& a, cudaStream_t s);
+cudaError_t launch_count_quantile(const TableBuildArgs& a, int64_t nnz, int64_t n_drop,
+                                  void* scratch, size_t scratch_bytes, cudaStream_t s);
+size_t count_quantile_scratch_bytes(int64_t nnz);
+size_t walk_smem_bytes_per_warp(int cap, int lanes, int log_stride);
+cudaError_t launch_walk(const WalkArgs& a, int warps_per_block, int num_sms, cudaStream_t s);
+
+// Exclusive scans (assemble.cu).
+size_t scan_scratch_bytes(int64_t n);
+cudaError_t scan_u32_exclusive(const unsigned* in, unsigned* out, int64_t n, void* scratch,
+                               cudaStream_t s);  // out[n] = total
+cudaError_t scan_rows_exclusive(const int* in, int64_t* out, int64_t n, void* scratch,
+                                cudaStream_t s);  // out[n] = total
+cudaError_t launch_compact(const int* stage_col, const double* stage_val, const int64_t* row_src,
+                           const int* row_cnt, const int64_t* row_ptr, int64_t rows,
+                           int64_t* col_out, double* val_out, cudaStream_t s);
+
+}  // namespace mcmi

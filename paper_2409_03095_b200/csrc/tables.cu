@@ -1,0 +1,341 @@
+// tables.cu — subsystem (1): drop filter, diagonal augmentation / splitting and
+// the per-state transition tables, all on device.
+//
+// Reference semantics (paths relative to /root/reference/proj):
+//   drop_small_entries      src/csr.cpp:127-157 (off_diagonal_range :88-105,
+//                           filter_entries :109-123)
+//   augment_and_split       src/split.cpp:46-100 (with_explicit_diagonal :10-42,
+//                           inf_norm csr.cpp:77-86)
+//   transition_probabilities src/split.cpp:102-119
+//   sample_transition's CDF src/mc_engine.cpp:64-78
+//
+// Every per-row floating-point sum is a sequential left fold in stored order
+// (one thread per row), exactly like the reference loops; maxima and minima
+// are order-independent and use integer atomics on the bit patterns.  With
+// -fmad=false every value here is bit-identical to the reference's.
+//
+// HBM layout produced (B200, 180 GB):
+//   desc[n]     uint2  {begin, deg}           8 B per state
+//   ent[nnz_A]  double2 {cum, a/p}           16 B per transition
+//   col[nnz_A]  int32                         4 B per transition
+//   b1_diag[n]  f64                           8 B per state
+// A step from state s reads desc[s] (1 sector), ent[begin .. k] (sequential)
+// and col[k]: the 20 + 8*deg(s) algorithmic bytes of SURVEY.md §8(d).
+#include <climits>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace mcmi {
+namespace {
+
+constexpr int TB = 256;
+
+inline int grid_for(int64_t items, int per_block = TB) {
+    int64_t g = (items + per_block - 1) / per_block;
+    if (g < 1) g = 1;
+    if (g > 148 * 64) g = 148 * 64;  // grid-stride beyond ~64 blocks per SM
+    return static_cast<int>(g);
+}
+
+__device__ __forceinline__ double drop_threshold(const Reductions* red, double p) {
+    const double mn = __longlong_as_double(static_cast<long long>(red->offmin_bits));
+    const double mx = __longlong_as_double(static_cast<long long>(red->offmax_bits));
+    return mn + p * (mx - mn);  // csr.cpp:136, no contraction (-fmad=false)
+}
+
+// Entry filter of drop_small_entries, evaluated in place.
+struct Keep {
+    int mode;           // -1 keep all, 0 value_range, 1 count_quantile (flags)
+    double threshold;   // value_range
+    const unsigned char* flags;
+    __device__ __forceinline__ bool operator()(int64_t i, int64_t k, int64_t c, double v) const {
+        if (mode < 0 || c == i) return true;  // diagonal is never dropped
+        if (mode == 0) return !(fabs(v) < threshold);
+        return flags[k] != 0;
+    }
+};
+
+__device__ __forceinline__ Keep make_keep(const TableBuildArgs& a) {
+    Keep kp;
+    kp.mode = -1;
+    kp.threshold = 0.0;
+    kp.flags = a.keep;
+    if (a.drop_fraction != 0.0) {
+        if (a.drop_mode == 0) {
+            // max_abs == 0 -> copy (csr.cpp:135)
+            if (a.red->offmax_bits != 0ull) {
+                kp.mode = 0;
+                kp.threshold = drop_threshold(a.red, a.drop_fraction);
+            }
+        } else if (a.keep != nullptr) {
+            kp.mode = 1;
+        }
+    }
+    return kp;
+}
+
+// off_diagonal_range (csr.cpp:88-105).
+__global__ void k_offdiag_range(TableBuildArgs a) {
+    double mn = __longlong_as_double(0x7ff0000000000000ll), mx = 0.0;
+    bool seen = false;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        for (int64_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
+            if (a.col_idx[k] == i) continue;
+            const double v = fabs(a.values[k]);
+            mn = fmin(mn, v);
+            mx = fmax(mx, v);
+            seen = true;
+        }
+    }
+    if (seen) {
+        atomic_min_nonneg(&a.red->offmin_bits, mn);
+        atomic_max_nonneg(&a.red->offmax_bits, mx);
+    }
+}
+
+// Pass B: ||B_reduced||inf, explicit diagonal value, column range check.
+__global__ void k_rows_norm(TableBuildArgs a) {
+    const Keep keep = make_keep(a);
+    double best = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0, d = 0.0;
+        bool found = false;
+        for (int64_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
+            const int64_t c = a.col_idx[k];
+            const double v = a.values[k];
+            if (c < 0 || c >= a.n) {
+                atomicMin(&a.red->bad_col_row, static_cast<long long>(i));
+                continue;
+            }
+            if (!keep(i, k, c, v)) continue;
+            s += fabs(v);  // inf_norm: sequential row sum (csr.cpp:80-83)
+            if (c == i && !found) {  // with_explicit_diagonal: missing -> 0 (split.cpp:10-42)
+                d = v;
+                found = true;
+            }
+        }
+        a.diag_val[i] = d;
+        best = fmax(best, s);
+    }
+    atomic_max_nonneg(&a.red->bnorm_bits, best);
+}
+
+// Pass C: B1 = diag(B_hat), A's row counts, ||A||inf, max degree.
+__global__ void k_rows_split(TableBuildArgs a) {
+    const Keep keep = make_keep(a);
+    const double b_norm = __longlong_as_double(static_cast<long long>(a.red->bnorm_bits));
+    double best = 0.0;
+    unsigned max_deg = 0;
+    unsigned long long nnz_a = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double d = a.diag_val[i];
+        double shift = a.alpha * b_norm;  // split.cpp:62-63
+        if (a.mode == 1 && d < 0.0) shift = -shift;
+        const double b1 = d + shift;
+        a.b1_diag[i] = b1;
+        if (b1 == 0.0) atomicMin(&a.red->degenerate_row, static_cast<long long>(i));
+        double row_sum = 0.0;
+        unsigned cnt = 0;
+        for (int64_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
+            const int64_t c = a.col_idx[k];
+            const double v = a.values[k];
+            if (c == i || c < 0 || c >= a.n || !keep(i, k, c, v)) continue;
+            const double av = -v / b1;  // split.cpp:82
+            if (av == 0.0) continue;
+            ++cnt;
+            row_sum += fabs(av);
+        }
+        a.a_cnt[i] = cnt;
+        best = fmax(best, row_sum);
+        max_deg = max(max_deg, cnt);
+        nnz_a += cnt;
+    }
+    atomic_max_nonneg(&a.red->anorm_bits, best);
+    atomicMax(&a.red->max_deg, static_cast<unsigned long long>(max_deg));
+    atomicAdd(&a.red->a_nnz, nnz_a);
+}
+
+// Pass D: transition records (split.cpp:75-92 values, split.cpp:102-119
+// probabilities, mc_engine.cpp:71-75 running CDF, mc_engine.cpp:94 ratio).
+__global__ void k_rows_fill(TableBuildArgs a) {
+    const Keep keep = make_keep(a);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double b1 = a.b1_diag[i];
+        const unsigned begin = a.a_off[i];
+        const unsigned cnt = a.a_cnt[i];
+        a.desc[i] = make_uint2(begin, cnt);
+        if (cnt == 0) continue;
+        const int64_t k0 = a.row_ptr[i], k1 = a.row_ptr[i + 1];
+        double row_sum = 0.0;  // transition_probabilities' sum == split's row_sum
+        for (int64_t k = k0; k < k1; ++k) {
+            const int64_t c = a.col_idx[k];
+            const double v = a.values[k];
+            if (c == i || c < 0 || c >= a.n || !keep(i, k, c, v)) continue;
+            const double av = -v / b1;
+            if (av == 0.0) continue;
+            row_sum += fabs(av);
+        }
+        double cum = 0.0;
+        unsigned o = begin;
+        for (int64_t k = k0; k < k1; ++k) {
+            const int64_t c = a.col_idx[k];
+            const double v = a.values[k];
+            if (c == i || c < 0 || c >= a.n || !keep(i, k, c, v)) continue;
+            const double av = -v / b1;
+            if (av == 0.0) continue;
+            const double p = fabs(av) / row_sum;
+            cum += p;
+            a.ent[o] = make_double2(cum, av / p);
+            a.col[o] = static_cast<int>(c);
+            ++o;
+        }
+    }
+}
+
+// ---- count-quantile drop (csr.cpp:138-155): radix select of the n_drop-th
+// smallest |b_ij| over off-diagonals, ties resolved by entry position.
+
+struct CqState {
+    unsigned long long prefix, mask, target, count_less, n_drop, n_off;
+    unsigned hist[256];
+};
+
+__global__ void k_cq_count(TableBuildArgs a, CqState* st) {
+    unsigned long long cnt = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) cnt += (a.col_idx[k] != i);
+    atomicAdd(&st->n_off, cnt);
+}
+
+__global__ void k_cq_init(CqState* st, double p) {
+    // n_drop = static_cast<size_t>(p * static_cast<double>(off.size())) (csr.cpp:145-146)
+    st->n_drop = static_cast<unsigned long long>(p * static_cast<double>(st->n_off));
+    st->target = st->n_drop;
+    st->prefix = 0;
+    st->mask = 0;
+    st->count_less = 0;
+    for (int b = 0; b < 256; ++b) st->hist[b] = 0;
+}
+
+__global__ void k_cq_hist(TableBuildArgs a, CqState* st, int shift) {
+    __shared__ unsigned h[256];
+    for (int b = threadIdx.x; b < 256; b += blockDim.x) h[b] = 0;
+    __syncthreads();
+    if (st->target != 0) {
+        const unsigned long long prefix = st->prefix, mask = st->mask;
+        for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+             i += (int64_t)gridDim.x * blockDim.x)
+            for (int64_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
+                if (a.col_idx[k] == i) continue;
+                const unsigned long long key =
+                    static_cast<unsigned long long>(__double_as_longlong(fabs(a.values[k])));
+                if ((key & mask) == prefix) atomicAdd(&h[(key >> shift) & 255u], 1u);
+            }
+    }
+    __syncthreads();
+    for (int b = threadIdx.x; b < 256; b += blockDim.x)
+        if (h[b]) atomicAdd(&st->hist[b], h[b]);
+}
+
+__global__ void k_cq_select(CqState* st, int shift) {
+    if (threadIdx.x != 0 || st->target == 0) return;
+    unsigned long long before = 0;
+    int b = 0;
+    for (; b < 256; ++b) {
+        if (before + st->hist[b] >= st->target) break;
+        before += st->hist[b];
+    }
+    st->count_less += before;
+    st->target -= before;
+    st->prefix |= static_cast<unsigned long long>(b) << shift;
+    st->mask |= 255ull << shift;
+    for (int q = 0; q < 256; ++q) st->hist[q] = 0;
+}
+
+// tie[k] = off-diagonal entry whose |v| equals the selected threshold.
+__global__ void k_cq_ties(TableBuildArgs a, const CqState* st, unsigned* tie) {
+    const unsigned long long thr = st->prefix;
+    const bool any = st->n_drop != 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
+            const unsigned long long key =
+                static_cast<unsigned long long>(__double_as_longlong(fabs(a.values[k])));
+            tie[k] = (any && a.col_idx[k] != i && key == thr) ? 1u : 0u;
+        }
+}
+
+__global__ void k_cq_keep(TableBuildArgs a, const CqState* st, const unsigned* tie_rank) {
+    const unsigned long long thr = st->prefix;
+    const bool any = st->n_drop != 0;
+    const unsigned long long ties = st->n_drop - st->count_less;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        for (int64_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
+            const unsigned long long key =
+                static_cast<unsigned long long>(__double_as_longlong(fabs(a.values[k])));
+            bool drop = false;
+            if (any && a.col_idx[k] != i)
+                drop = key < thr || (key == thr && tie_rank[k] < ties);
+            a.keep[k] = drop ? 0 : 1;
+        }
+}
+
+}  // namespace
+
+size_t count_quantile_scratch_bytes(int64_t nnz) {
+    const size_t align = 256;
+    size_t b = (sizeof(CqState) + align - 1) / align * align;
+    b += (static_cast<size_t>(nnz) + 1) * sizeof(unsigned) * 2 + 2 * align;  // tie, tie_rank
+    b += scan_scratch_bytes(nnz) + align;
+    return b;
+}
+
+cudaError_t launch_count_quantile(const TableBuildArgs& a, int64_t nnz, int64_t /*n_drop*/,
+                                  void* scratch, size_t /*scratch_bytes*/, cudaStream_t s) {
+    auto* base = static_cast<unsigned char*>(scratch);
+    const size_t align = 256;
+    CqState* st = reinterpret_cast<CqState*>(base);
+    size_t off = (sizeof(CqState) + align - 1) / align * align;
+    unsigned* tie = reinterpret_cast<unsigned*>(base + off);
+    off += ((static_cast<size_t>(nnz) + 1) * sizeof(unsigned) + align - 1) / align * align;
+    unsigned* tie_rank = reinterpret_cast<unsigned*>(base + off);
+    off += ((static_cast<size_t>(nnz) + 1) * sizeof(unsigned) + align - 1) / align * align;
+    void* scan_tmp = base + off;
+
+    cudaMemsetAsync(st, 0, sizeof(CqState), s);
+    const int g = grid_for(a.n);
+    k_cq_count<<<g, TB, 0, s>>>(a, st);
+    k_cq_init<<<1, 1, 0, s>>>(st, a.drop_fraction);
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        k_cq_hist<<<g, TB, 0, s>>>(a, st, shift);
+        k_cq_select<<<1, 32, 0, s>>>(st, shift);
+    }
+    k_cq_ties<<<g, TB, 0, s>>>(a, st, tie);
+    cudaError_t e = scan_u32_exclusive(tie, tie_rank, nnz, scan_tmp, s);
+    if (e != cudaSuccess) return e;
+    k_cq_keep<<<g, TB, 0, s>>>(a, st, tie_rank);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_table_build(const TableBuildArgs& a, int64_t /*nnz*/, bool drop_active,
+                               cudaStream_t s) {
+    const int g = grid_for(a.n);
+    if (drop_active && a.drop_mode == 0) k_offdiag_range<<<g, TB, 0, s>>>(a);
+    k_rows_norm<<<g, TB, 0, s>>>(a);
+    k_rows_split<<<g, TB, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_table_fill(const TableBuildArgs& a, cudaStream_t s) {
+    k_rows_fill<<<grid_for(a.n), TB, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace mcmi

@@ -1,0 +1,472 @@
+// walk.cu — subsystems (2) random walks and (3) per-row accumulate / top-k /
+// scale / prune, fused in one persistent warp-per-row kernel.
+//
+// Reference: estimate_row_impl (mc_engine.cpp:80-113), sample_transition
+// (:64-78), retain_top_k (:124-145), scale_columns (:147-149), the zero prune
+// (:174-176) and RowMeta (:169).
+//
+// Scheduling: one warp owns one row at a time (rows claimed in index order
+// from a global cursor, so concurrently walked rows are neighbours and their
+// transition records stay L1/L2-resident).  The 32 lanes run 32 chains of the
+// row concurrently ("batch"), so the dependent gathers of 32 walks overlap.
+//
+// RNG keying (WalkArgs::rng_mode):
+//   MCMI_RNG_REFERENCE: RngStream(seed, row) with draws numbered across
+//     chains (rng.hpp:17-74).  Chain c starts at draw D_c = D_{c-1} + k(D_{c-1}),
+//     where k(d) = draws consumed by a walk whose first draw is d — the same
+//     function for every chain of the row.  Lane j speculatively walks from
+//     D + j*ell; the lanes on the orbit of D (found by pointer doubling over
+//     next(j) = j + k_j/ell) are exactly the reference's chains, the rest are
+//     discarded.  ell adapts to the observed draws per chain, so a row whose
+//     chains all draw the same number of times (the common case) wastes nothing.
+//   MCMI_RNG_KEYED: u(row, chain, step) = double #(step&1) of
+//     Philox({step>>1, chain, row lo, row hi}, seed); every lane is a chain.
+//
+// Accumulation order: the reference adds deposits to acc[col] in (chain, step)
+// order (RowWorkspace::deposit, mc_engine.cpp:45-51).  Floating-point addition
+// is not associative, so each batch logs its deposits [lane][step] in shared
+// memory and folds them chain-major: per 32-entry chunk, __match_any_sync
+// groups equal columns and the group leader adds its peers in lane order.  The
+// per-column sums are therefore bit-identical to the reference's.
+//
+// Accumulator: an open-addressing hash (int32 column -> f64 sum) per warp in
+// shared memory, capacity `cap`; a row that touches more than cap_limit
+// columns is abandoned and re-run by the host on a larger tier.
+//
+// Finalize (per row, in shared memory): compact the hash, bitonic-sort by
+// column, multiply by 1/chains_run, rank for retain_top_k (diag first, |v|
+// desc, col asc), divide by b1_diag[col], prune exact zeros off the diagonal,
+// write the row to its staging slot.
+#include <climits>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace mcmi {
+namespace {
+
+__host__ __device__ inline int round32(int x) { return (x + 31) & ~31; }
+
+struct WarpSmem {
+    double* vals;   // [cap]
+    double* log_w;  // [logn]
+    int* keys;      // [cap]
+    int* log_col;   // [logn]
+};
+
+__device__ __forceinline__ WarpSmem carve(unsigned char* base, int cap, int logn) {
+    WarpSmem s;
+    s.vals = reinterpret_cast<double*>(base);
+    s.log_w = s.vals + cap;
+    s.keys = reinterpret_cast<int*>(s.log_w + logn);
+    s.log_col = s.keys + cap;
+    return s;
+}
+
+// Insert-or-find; returns the slot or -1 if the table is full.
+__device__ __forceinline__ int hash_slot(int* keys, unsigned mask, int shift, int col,
+                                         int& n_new) {
+    unsigned h = (static_cast<unsigned>(col) * 0x9E3779B1u) >> shift;
+    volatile int* vk = keys;
+    for (unsigned probe = 0; probe <= mask; ++probe) {
+        const int k = vk[h];
+        if (k == col) return static_cast<int>(h);
+        if (k == EMPTY_KEY) {
+            const int old = atomicCAS(&keys[h], EMPTY_KEY, col);
+            if (old == EMPTY_KEY) {
+                ++n_new;
+                return static_cast<int>(h);
+            }
+            if (old == col) return static_cast<int>(h);
+        }
+        h = (h + 1) & mask;
+    }
+    return -1;
+}
+
+__device__ __forceinline__ int warp_sum_int(int v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+    return v;
+}
+
+// retain_top_k ordering (mc_engine.cpp:131-139): does entry j precede entry i?
+__device__ __forceinline__ bool topk_before(int cj, double vj, int ci, double vi, int diag) {
+    const bool dj = cj == diag, di = ci == diag;
+    if (dj != di) return dj;
+    const double mj = fabs(vj), mi = fabs(vi);
+    if (mj != mi) return mj > mi;
+    return cj < ci;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(256) k_walk(const WalkArgs a) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = static_cast<int>(threadIdx.x & 31);
+    const int warp = static_cast<int>(threadIdx.x >> 5);
+    const int cap = a.cap;
+    const int S = a.log_stride;                 // deposits per chain: W0 + max_len
+    const int B = a.lanes;                      // chains per batch
+    const int logn = round32(B * S);
+    const size_t per_warp = static_cast<size_t>(cap + logn) * 12;
+    const WarpSmem sm = carve(smem_raw + per_warp * warp, cap, logn);
+    const unsigned cap_mask = static_cast<unsigned>(cap - 1);
+    const int shift = 32 - (31 - __clz(cap));
+    const unsigned lt_mask = (1u << lane) - 1u;
+
+    const uint2* __restrict__ desc = a.t.desc;
+    const double2* __restrict__ ent = a.t.ent;
+    const int* __restrict__ tcol = a.t.col;
+    const uint2 key = make_uint2(static_cast<uint32_t>(a.seed), static_cast<uint32_t>(a.seed >> 32));
+    const int64_t N = a.n_chains;
+    const int64_t L = a.max_len;
+
+    unsigned long long tot_steps = 0, tot_deg = 0;
+
+    for (;;) {
+        long long wi = 0;
+        if (lane == 0) wi = static_cast<long long>(atomicAdd(&a.counters[0], 1ull));
+        wi = __shfl_sync(FULL_MASK, wi, 0);
+        if (wi >= a.n_work) break;
+        const int64_t row = a.row_list ? static_cast<int64_t>(a.row_list[wi]) : a.row_begin + wi;
+        const int rowc = static_cast<int>(row);
+
+        for (int i = lane; i < cap; i += 32) {
+            sm.keys[i] = EMPTY_KEY;
+            sm.vals[i] = 0.0;
+        }
+        __syncwarp();
+
+        int distinct = 0;
+        bool overflow = false;
+        int64_t chains_done = 0;
+        int64_t chains_run = N;
+        unsigned long long row_steps = 0, row_deg = 0;
+        // reference-stream speculation state
+        unsigned long long D = 0;
+        unsigned long long ell = static_cast<unsigned long long>(a.ell0);
+        bool row_done = false;
+
+        while (!row_done) {
+            // ------------------------------------------------ walk one batch
+            bool active;
+            unsigned long long pos = 0;  // next draw index (reference stream)
+            int64_t chain = 0;           // chain index (keyed)
+            if (MODE == 0) {
+                active = lane < B;
+                pos = D + static_cast<unsigned long long>(lane) * ell;
+            } else {
+                chain = chains_done + lane;
+                active = lane < B && chain < N;
+            }
+            int* lc = sm.log_col + lane * S;
+            double* lw = sm.log_w + lane * S;
+            int m = 0;
+            if (active) {
+                lc[0] = rowc;  // W0 = 1 lands on (r, r) (mc_engine.cpp:89)
+                lw[0] = 1.0;
+                m = 1;
+            }
+            int state = rowc;
+            double w = 1.0;
+            unsigned long long draws = 0;
+            unsigned long long cached = ~0ull;
+            uint4 blk = make_uint4(0, 0, 0, 0);
+            bool alive = active;
+            for (int64_t t = 0; __any_sync(FULL_MASK, alive); ++t) {
+                if (alive && t >= L) alive = false;
+                if (!alive) continue;
+                const uint2 d = desc[state];
+                if (d.y == 0) {  // absorbing state (mc_engine.cpp:68)
+                    alive = false;
+                    continue;
+                }
+                ++row_steps;
+                row_deg += d.y;
+                unsigned k;
+                double ratio;
+                if (d.y == 1) {  // forced move, no draw (mc_engine.cpp:69)
+                    k = d.x;
+                    ratio = ent[k].y;
+                } else {
+                    double u;
+                    if (MODE == 0) {
+                        const unsigned long long b = pos >> 1;
+                        if (b != cached) {
+                            blk = philox4x32_10(
+                                make_uint4(static_cast<uint32_t>(b), static_cast<uint32_t>(b >> 32),
+                                           static_cast<uint32_t>(row),
+                                           static_cast<uint32_t>(static_cast<uint64_t>(row) >> 32)),
+                                key);
+                            cached = b;
+                        }
+                        u = (pos & 1) ? u32pair_to_double(blk.z, blk.w)
+                                      : u32pair_to_double(blk.x, blk.y);
+                        ++pos;
+                    } else {
+                        const unsigned long long b = static_cast<unsigned long long>(t) >> 1;
+                        if (b != cached) {
+                            blk = philox4x32_10(
+                                make_uint4(static_cast<uint32_t>(b), static_cast<uint32_t>(chain),
+                                           static_cast<uint32_t>(row),
+                                           static_cast<uint32_t>(static_cast<uint64_t>(row) >> 32)),
+                                key);
+                            cached = b;
+                        }
+                        u = (t & 1) ? u32pair_to_double(blk.z, blk.w)
+                                    : u32pair_to_double(blk.x, blk.y);
+                    }
+                    ++draws;
+                    // inverse CDF: first k with u < cum_k, else the last entry
+                    // (mc_engine.cpp:71-77)
+                    const unsigned end = d.x + d.y;
+                    k = end - 1;
+                    ratio = 0.0;
+                    for (unsigned q = d.x; q < end; ++q) {
+                        const double2 e = ent[q];
+                        ratio = e.y;
+                        if (u < e.x) {
+                            k = q;
+                            break;
+                        }
+                    }
+                }
+                w *= ratio;  // w *= a_k / p_k (mc_engine.cpp:94)
+                state = tcol[k];
+                lc[m] = state;
+                lw[m] = w;
+                ++m;
+                if (fabs(w) < a.delta) alive = false;  // mc_engine.cpp:97
+            }
+
+            // ------------------------------------------- which lanes count
+            unsigned valid;
+            const bool first = chains_done == 0;
+            const unsigned long long draws0 = __shfl_sync(FULL_MASK, draws, 0);
+            if (first && draws0 == 0) {
+                // chain 0 consumed no randomness: its single realization is the
+                // estimator mean (mc_engine.cpp:101-104)
+                valid = 1u;
+                chains_run = 1;
+                row_done = true;
+            } else if (MODE == 0) {
+                int nxt = lane;
+                if (active && draws > 0 && draws % ell == 0) {
+                    const unsigned long long q = draws / ell;
+                    if (static_cast<unsigned long long>(lane) + q < static_cast<unsigned long long>(B))
+                        nxt = lane + static_cast<int>(q);
+                }
+                unsigned R = (1u << lane) | (1u << nxt);
+                int J = nxt;
+#pragma unroll
+                for (int i = 0; i < 5; ++i) {
+                    const unsigned Rn = __shfl_sync(FULL_MASK, R, J);
+                    const int Jn = __shfl_sync(FULL_MASK, J, J);
+                    R |= Rn;
+                    J = Jn;
+                }
+                valid = __shfl_sync(FULL_MASK, R, 0);
+            } else {
+                valid = __ballot_sync(FULL_MASK, active);
+            }
+            const int64_t remaining = N - chains_done;
+            while (static_cast<int64_t>(__popc(valid)) > remaining)
+                valid &= ~(1u << (31 - __clz(valid)));
+            if (MODE == 0 && !row_done) {
+                const int lv = 31 - __clz(valid);
+                const unsigned long long klv = __shfl_sync(FULL_MASK, draws, lv);
+                D = D + static_cast<unsigned long long>(lv) * ell + klv;
+                ell = draws0 > 0 ? draws0 : 1ull;
+            }
+            __syncwarp();
+
+            // ------------------------------------- ordered (chain, step) fold
+            int n_new = 0;
+            bool fail = false;
+            const int span = B * S;
+            for (int base = 0; base < span; base += 32) {
+                const int p = base + lane;
+                int c = -1 - lane;  // unique non-column tag for empty positions
+                const int j = min(p / S, 31);
+                const int tt = p - j * S;
+                const int mj = __shfl_sync(FULL_MASK, m, j);
+                const bool ok = p < span && ((valid >> j) & 1u) && tt < mj;
+                if (ok) c = sm.log_col[p];
+                const unsigned peers = __match_any_sync(FULL_MASK, c);
+                if (ok && (__ffs(peers) - 1) == lane) {
+                    const int slot = hash_slot(sm.keys, cap_mask, shift, c, n_new);
+                    if (slot < 0) {
+                        fail = true;
+                    } else {
+                        double v = sm.vals[slot];
+                        unsigned rest = peers;
+                        while (rest) {
+                            const int b = __ffs(rest) - 1;
+                            rest &= rest - 1;
+                            v += sm.log_w[base + b];
+                        }
+                        sm.vals[slot] = v;
+                    }
+                }
+                __syncwarp();
+            }
+            distinct += warp_sum_int(n_new);
+            if (__any_sync(FULL_MASK, fail) || distinct > a.cap_limit) {
+                overflow = true;
+                break;
+            }
+            chains_done += __popc(valid);
+            if (chains_done >= N) row_done = true;
+        }
+
+        const int64_t lrow = row - a.row_begin;
+        if (overflow) {
+            if (lane == 0) {
+                const unsigned long long q = atomicAdd(&a.counters[3], 1ull);
+                a.overflow_list[q] = rowc;
+            }
+            continue;
+        }
+        tot_steps += row_steps;
+        tot_deg += row_deg;
+
+        // ------------------------------------------------------ finalize
+        // compact occupied slots to [0, distinct) (in place, order-preserving)
+        int o = 0;
+        for (int i0 = 0; i0 < cap; i0 += 32) {
+            const int i = i0 + lane;
+            const int kk = sm.keys[i];
+            const double vv = sm.vals[i];
+            const bool occ = kk != EMPTY_KEY;
+            const unsigned bal = __ballot_sync(FULL_MASK, occ);
+            __syncwarp();
+            if (occ) {
+                const int dst = o + __popc(bal & lt_mask);
+                sm.keys[dst] = kk;
+                sm.vals[dst] = vv;
+            }
+            o += __popc(bal);
+            __syncwarp();
+        }
+        const int s = distinct;
+        int P = 32;
+        while (P < s) P <<= 1;
+        for (int i = s + lane; i < P; i += 32) {
+            sm.keys[i] = INT_MAX;
+            sm.vals[i] = 0.0;
+        }
+        __syncwarp();
+        // bitonic sort by column
+        for (int kb = 2; kb <= P; kb <<= 1) {
+            for (int jb = kb >> 1; jb > 0; jb >>= 1) {
+                for (int i = lane; i < P; i += 32) {
+                    const int ixj = i ^ jb;
+                    if (ixj > i) {
+                        const int ka = sm.keys[i], kc = sm.keys[ixj];
+                        const bool up = (i & kb) == 0;
+                        if ((ka > kc) == up) {
+                            const double va = sm.vals[i];
+                            sm.keys[i] = kc;
+                            sm.keys[ixj] = ka;
+                            sm.vals[i] = sm.vals[ixj];
+                            sm.vals[ixj] = va;
+                        }
+                    }
+                }
+                __syncwarp();
+            }
+        }
+        const double inv_n = 1.0 / static_cast<double>(chains_run);  // mc_engine.cpp:109
+        for (int i = lane; i < s; i += 32) sm.vals[i] = sm.vals[i] * inv_n;
+        __syncwarp();
+
+        const bool keep_all = a.retain_k <= 0 || static_cast<int64_t>(s) <= a.retain_k;
+        const int64_t out_off = a.stage_base + wi * a.stage_stride;
+        int* __restrict__ oc = a.stage_col + out_off;
+        double* __restrict__ ov = a.stage_val + out_off;
+        int n_out = 0;
+        for (int i0 = 0; i0 < s; i0 += 32) {
+            const int i = i0 + lane;
+            bool keep = i < s;
+            int c = 0;
+            double v = 0.0;
+            if (keep) {
+                c = sm.keys[i];
+                v = sm.vals[i];
+                if (!keep_all) {
+                    int64_t rank = 0;
+                    for (int j = 0; j < s; ++j) rank += topk_before(sm.keys[j], sm.vals[j], c, v, rowc);
+                    keep = rank < a.retain_k;
+                }
+            }
+            if (keep) {
+                v = v / a.t.b1_diag[c];                // scale_columns (mc_engine.cpp:148)
+                keep = !(v == 0.0 && c != rowc);       // prune (mc_engine.cpp:174-176)
+            }
+            const unsigned bal = __ballot_sync(FULL_MASK, keep);
+            if (keep) {
+                const int dst = n_out + __popc(bal & lt_mask);
+                oc[dst] = c;
+                ov[dst] = v;
+            }
+            n_out += __popc(bal);
+        }
+        if (lane == 0) {
+            a.row_cnt[lrow] = n_out;
+            a.row_src[lrow] = out_off;
+            a.chains_used[lrow] = chains_run;
+            a.entries_before[lrow] = s;
+        }
+        __syncwarp();
+    }
+
+    tot_steps = warp_sum_u64(tot_steps);
+    tot_deg = warp_sum_u64(tot_deg);
+    if (lane == 0) {
+        atomicAdd(&a.counters[1], tot_steps);
+        atomicAdd(&a.counters[2], tot_deg);
+    }
+}
+
+}  // namespace
+
+size_t walk_smem_bytes_per_warp(int cap, int lanes, int log_stride) {
+    return static_cast<size_t>(cap + round32(lanes * log_stride)) * 12;
+}
+
+cudaError_t launch_walk(const WalkArgs& a, int warps_per_block, int num_sms, cudaStream_t s) {
+    if (a.n_work <= 0) return cudaSuccess;
+    const size_t smem = walk_smem_bytes_per_warp(a.cap, a.lanes, a.log_stride) * warps_per_block;
+    const int threads = warps_per_block * 32;
+    int per_sm = 0;
+    cudaError_t e;
+    if (a.rng_mode == 0) {
+        e = cudaFuncSetAttribute(k_walk<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<0>, threads, smem);
+    } else {
+        e = cudaFuncSetAttribute(k_walk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem));
+        if (e != cudaSuccess) return e;
+        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<1>, threads, smem);
+    }
+    if (e != cudaSuccess) return e;
+    if (per_sm < 1) return cudaErrorInvalidConfiguration;
+    int64_t blocks = static_cast<int64_t>(per_sm) * num_sms;
+    const int64_t need = (a.n_work + warps_per_block - 1) / warps_per_block;
+    if (blocks > need) blocks = need;
+    if (a.rng_mode == 0)
+        k_walk<0><<<static_cast<unsigned>(blocks), threads, smem, s>>>(a);
+    else
+        k_walk<1><<<static_cast<unsigned>(blocks), threads, smem, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace mcmi

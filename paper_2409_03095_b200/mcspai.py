@@ -1,0 +1,255 @@
+"""Python mirror of the reference's preconditioner-build interface.
+
+Same names, argument meaning and error behaviour as
+``/root/reference/proj/include/mcspai/mc_engine.hpp`` and ``split.hpp`` /
+``csr.hpp``, so the parity tests read like the reference's own tests:
+
+=========================  ===============================================
+reference (C++)            here
+=========================  ===============================================
+``McConfig``               :class:`McConfig` (+ ``rng_mode``, ``device``)
+``CsrMatrix``              :class:`CsrMatrix` (int64 / float64 numpy)
+``ApproxInverse``          :class:`ApproxInverse`
+``RowMeta``                :class:`RowMeta` (column arrays)
+``ChainBudget``            :class:`ChainBudget`
+``compute_preconditioner`` :func:`compute_preconditioner`
+``std::invalid_argument``  :class:`ValueError`
+``SplitError``             :class:`SplitError`
+``std::out_of_range``      :class:`IndexError`
+=========================  ===============================================
+
+Every call goes through the C-ABI (include/mcmi.h) into the sm_100a kernels.
+``n_threads`` is accepted for signature compatibility; the device count of a
+sharded build is chosen by :mod:`paper_2409_03095_b200.distributed`.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from enum import IntEnum
+from typing import Optional
+
+import numpy as np
+
+from . import _lib as L
+
+index_t = np.int64
+
+
+class AugmentationMode(IntEnum):  # split.hpp:9-12
+    plain = 0
+    sign_aware = 1
+
+
+class DropMode(IntEnum):  # csr.hpp:61-64
+    value_range = 0
+    count_quantile = 1
+
+
+class RngMode(IntEnum):
+    reference = 0  #: RngStream(seed, row): byte-identical to the reference
+    keyed = 1  #: Philox keyed by (row, chain, step)
+
+
+class SplitError(RuntimeError):
+    """mcspai::SplitError (split.hpp:14-16)."""
+
+
+class DeviceError(RuntimeError):
+    """CUDA runtime / device failure (no CPU fallback exists)."""
+
+
+@dataclass
+class McConfig:  # mc_engine.hpp:15-26
+    epsilon: float = 0.0625
+    delta: float = 0.0625
+    alpha: float = 5.0
+    mode: AugmentationMode = AugmentationMode.sign_aware
+    drop_fraction: float = 0.0
+    drop_mode: DropMode = DropMode.value_range
+    retain_k: int = 0
+    chains_override: Optional[int] = None
+    max_len_override: Optional[int] = None
+    master_seed: int = 0
+    rng_mode: RngMode = RngMode.reference
+    device: int = 0
+
+    def to_c(self) -> L.mcmi_config:
+        c = L.mcmi_config()
+        c.epsilon = float(self.epsilon)
+        c.delta = float(self.delta)
+        c.alpha = float(self.alpha)
+        c.mode = int(self.mode)
+        c.drop_mode = int(self.drop_mode)
+        c.drop_fraction = float(self.drop_fraction)
+        c.retain_k = int(self.retain_k)
+        c.has_chains_override = int(self.chains_override is not None)
+        c.chains_override = int(self.chains_override or 0)
+        c.has_max_len_override = int(self.max_len_override is not None)
+        c.max_len_override = int(self.max_len_override or 0)
+        c.master_seed = int(self.master_seed) & 0xFFFFFFFFFFFFFFFF
+        c.rng_mode = int(self.rng_mode)
+        c.device = int(self.device)
+        return c
+
+    def oracle_kwargs(self) -> dict:
+        """Field dict accepted by oracle.make_config / ref.make_config (tests)."""
+        return dict(epsilon=self.epsilon, delta=self.delta, alpha=self.alpha, mode=int(self.mode),
+                    drop_fraction=self.drop_fraction, drop_mode=int(self.drop_mode),
+                    retain_k=int(self.retain_k), chains_override=self.chains_override,
+                    max_len_override=self.max_len_override, master_seed=int(self.master_seed),
+                    rng_mode=int(self.rng_mode))
+
+
+@dataclass
+class CsrMatrix:  # csr.hpp:16-40
+    n: int = 0
+    row_ptr: np.ndarray = field(default_factory=lambda: np.zeros(1, np.int64))
+    col_idx: np.ndarray = field(default_factory=lambda: np.zeros(0, np.int64))
+    values: np.ndarray = field(default_factory=lambda: np.zeros(0, np.float64))
+
+    def __post_init__(self):
+        self.row_ptr = np.ascontiguousarray(self.row_ptr, dtype=np.int64)
+        self.col_idx = np.ascontiguousarray(self.col_idx, dtype=np.int64)
+        self.values = np.ascontiguousarray(self.values, dtype=np.float64)
+
+    def nnz(self) -> int:
+        return int(self.values.size)
+
+    def row_begin(self, i: int) -> int:
+        return int(self.row_ptr[i])
+
+    def row_end(self, i: int) -> int:
+        return int(self.row_ptr[i + 1])
+
+    def at(self, i: int, j: int) -> float:
+        a, b = self.row_ptr[i], self.row_ptr[i + 1]
+        k = a + np.searchsorted(self.col_idx[a:b], j)
+        return float(self.values[k]) if k < b and self.col_idx[k] == j else 0.0
+
+    def __eq__(self, other) -> bool:  # `operator== = default`
+        return (isinstance(other, CsrMatrix) and self.n == other.n
+                and np.array_equal(self.row_ptr, other.row_ptr)
+                and np.array_equal(self.col_idx, other.col_idx)
+                and np.array_equal(self.values.view(np.uint64), other.values.view(np.uint64)))
+
+    @staticmethod
+    def identity(n: int) -> "CsrMatrix":
+        return CsrMatrix(n, np.arange(n + 1), np.arange(n), np.ones(n))
+
+    @staticmethod
+    def from_triplets(n, rows, cols, vals) -> "CsrMatrix":
+        """csr.cpp:17-58: sort by (row, col), sum duplicates, prune exact zeros."""
+        rows = np.asarray(rows, np.int64)
+        cols = np.asarray(cols, np.int64)
+        vals = np.asarray(vals, np.float64)
+        if not (rows.size == cols.size == vals.size):
+            raise ValueError("triplet arrays must have equal length")
+        if rows.size and (rows.min() < 0 or rows.max() >= n or cols.min() < 0 or cols.max() >= n):
+            raise IndexError("triplet index out of range")
+        order = np.lexsort((cols, rows))  # stable
+        r, c, v = rows[order], cols[order], vals[order]
+        if r.size:
+            new = np.ones(r.size, bool)
+            new[1:] = (r[1:] != r[:-1]) | (c[1:] != c[:-1])
+            starts = np.flatnonzero(new)
+            # duplicates are summed in stored order (left fold)
+            sums = np.array([_fold(v[s:e]) for s, e in zip(starts, list(starts[1:]) + [r.size])]) \
+                if (~new).any() else v[starts]
+            r, c, v = r[starts], c[starts], sums
+            keep = v != 0.0
+            r, c, v = r[keep], c[keep], v[keep]
+        rp = np.zeros(n + 1, np.int64)
+        np.add.at(rp, r + 1, 1)
+        return CsrMatrix(n, np.cumsum(rp), c, v)
+
+
+def _fold(x):
+    s = 0.0
+    for t in x:
+        s += float(t)
+    return s
+
+
+@dataclass
+class ChainBudget:  # mc_engine.hpp:28-31
+    n_chains: int = 1
+    max_len: int = 1
+
+
+@dataclass
+class RowMeta:  # mc_engine.hpp:33-36, one array entry per row
+    chains_used: np.ndarray
+    entries_before_retention: np.ndarray
+
+
+@dataclass
+class ApproxInverse:  # mc_engine.hpp:39-45
+    m: CsrMatrix
+    row_meta: RowMeta
+    config_echo: McConfig
+    budget_echo: ChainBudget
+    seed_echo: int
+    stats: dict = field(default_factory=dict)
+
+
+def raise_for(code: int, msg: str):
+    if code == L.MCMI_OK:
+        return
+    if code == L.MCMI_EINVAL:
+        raise ValueError(msg)
+    if code == L.MCMI_ESPLIT:
+        raise SplitError(msg)
+    if code == L.MCMI_ERANGE:
+        raise IndexError(msg)
+    if code == L.MCMI_ENOMEM:
+        raise MemoryError(msg)
+    raise DeviceError(f"[status {code}] {msg}")
+
+
+def compute_preconditioner(b: CsrMatrix, cfg: McConfig | None = None, n_threads: int = 0,
+                           out: dict | None = None, rows: tuple[int, int] | None = None) -> ApproxInverse:
+    """mcspai::compute_preconditioner (mc_engine.hpp:80-81) on a B200.
+
+    ``out`` may hold preallocated (pinned) numpy arrays ``row_ptr``,
+    ``col_idx``, ``values`` of sufficient size to receive the result without
+    an extra allocation (used by the end-to-end benchmark).  ``rows`` =
+    (begin, end) builds only that row shard (``mcmi_build_rows``).
+    """
+    del n_threads
+    cfg = cfg or McConfig()
+    lib = L.load()
+    view = L.mcmi_csr_view(int(b.n), b.row_ptr.ctypes.data, b.col_idx.ctypes.data if b.col_idx.size else None,
+                           b.values.ctypes.data if b.values.size else None)
+    c = cfg.to_c()
+    h = C.c_void_p()
+    err = C.create_string_buffer(1024)
+    lo, hi = rows if rows is not None else (0, -1)
+    code = lib.mcmi_build_rows(C.byref(view), C.byref(c), lo, hi, C.byref(h), err, 1024)
+    raise_for(code, err.value.decode(errors="replace"))
+    try:
+        n, nnz = C.c_int64(), C.c_int64()
+        lib.mcmi_result_sizes(h, C.byref(n), C.byref(nnz))
+        n, nnz = n.value, nnz.value
+        if out is not None and out.get("values") is not None and out["values"].size >= nnz:
+            rp, ci, v = out["row_ptr"][: n + 1], out["col_idx"][:nnz], out["values"][:nnz]
+        else:
+            rp, ci, v = np.empty(n + 1, np.int64), np.empty(nnz, np.int64), np.empty(nnz, np.float64)
+        cu, eb = np.empty(n, np.int64), np.empty(n, np.int64)
+        nc, ml = C.c_int64(), C.c_int64()
+        code = lib.mcmi_result_copy(h, rp.ctypes.data, ci.ctypes.data if nnz else None,
+                                    v.ctypes.data if nnz else None, cu.ctypes.data if n else None,
+                                    eb.ctypes.data if n else None, C.byref(nc), C.byref(ml))
+        raise_for(code, "result copy failed")
+        st = L.mcmi_stats()
+        lib.mcmi_result_stats(h, C.byref(st))
+    finally:
+        lib.mcmi_result_free(h)
+    return ApproxInverse(CsrMatrix(n, rp, ci, v), RowMeta(cu, eb), cfg, ChainBudget(nc.value, ml.value),
+                         int(cfg.master_seed), st.as_dict())
+
+
+def compute_preconditioner_serial(b: CsrMatrix, cfg: McConfig | None = None) -> ApproxInverse:
+    """The reference's serial twin (mc_engine.hpp:85-86): same contract, so
+    the same device build (the result is independent of execution layout)."""
+    return compute_preconditioner(b, cfg)

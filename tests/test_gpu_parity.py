@@ -1,0 +1,244 @@
+"""GPU parity: the sm_100a build through the C-ABI vs the reference.
+
+Tier 1 (bit-exact):
+  * rng_mode=reference: byte-identical Matrix Market output to the UNMODIFIED
+    reference on every golden case (sha256 recorded by make_goldens.py from
+    oracle/_ref), plus RowMeta and the chain budget.
+  * rng_mode=keyed: bit-identical to the CPU oracle's keyed restatement.
+  * Full-size configs (C2, C3, C4): sampled row windows bit-identical to the
+    oracle, which restates the whole split and walks only those rows.
+Tier 2 (Monte Carlo tolerance, stated here): keyed vs reference stream on the
+same input: ||M_K - M_R||_F / ||M_R||_F <= 0.3*eps, max |M_K - M_R| <= 0.5*eps*max|M_R|,
+||I - B_hat M||_F / sqrt(n) within 10% of the reference's.
+"""
+import numpy as np
+import pytest
+
+from helpers import arr_sha256, bits_equal, golden_input, goldens, mm_sha256
+
+pytestmark = pytest.mark.gpu
+
+GOLD = goldens()
+
+
+@pytest.fixture(scope="module")
+def mc():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2409_03095_b200 import mcspai
+    return mcspai
+
+
+def _csr(mc, spec):
+    n, rp, ci, v = golden_input(spec)
+    return mc.CsrMatrix(n, rp, ci, v)
+
+
+def _cfg(mc, d, **extra):
+    d = dict(d)
+    d.update(extra)
+    for k in ("mode", "drop_mode", "rng_mode"):
+        if k in d:
+            d[k] = int(d[k])
+    return mc.McConfig(**d)
+
+
+@pytest.mark.parametrize("name", sorted(GOLD))
+def test_reference_stream_byte_identical_to_reference(mc, name):
+    case = GOLD[name]
+    b = _csr(mc, case["input"])
+    inv = mc.compute_preconditioner(b, _cfg(mc, case["config"]))
+    assert inv.budget_echo.n_chains == case["n_chains"]
+    assert inv.budget_echo.max_len == case["max_len"]
+    assert inv.m.nnz() == case["nnz"]
+    assert mm_sha256(b.n, inv.m.row_ptr, inv.m.col_idx, inv.m.values) == case["mm_sha256"]
+    assert arr_sha256(inv.row_meta.chains_used) == case["chains_used_sha256"]
+    assert arr_sha256(inv.row_meta.entries_before_retention) == case["entries_before_sha256"]
+
+
+@pytest.mark.parametrize("name", sorted(GOLD))
+def test_keyed_bit_identical_to_oracle(mc, oracle_mod, name):
+    case = GOLD[name]
+    b = _csr(mc, case["input"])
+    cfg = _cfg(mc, case["config"], rng_mode=1)
+    inv = mc.compute_preconditioner(b, cfg)
+    want = oracle_mod.compute_preconditioner(b.n, b.row_ptr, b.col_idx, b.values, **cfg.oracle_kwargs())
+    assert np.array_equal(inv.m.row_ptr, want.row_ptr)
+    assert np.array_equal(inv.m.col_idx, want.col_idx)
+    assert bits_equal(inv.m.values, want.values)
+    assert np.array_equal(inv.row_meta.chains_used, want.chains_used)
+    assert np.array_equal(inv.row_meta.entries_before_retention, want.entries_before)
+    assert inv.stats["walk_steps"] == want.walk_steps
+    assert inv.stats["walk_deg_sum"] == want.walk_deg_sum
+
+
+@pytest.mark.parametrize("rng", [0, 1])
+def test_step_counters_match_oracle(mc, oracle_mod, rng):
+    b = _csr(mc, "convdiff:100:0:0")
+    inv = mc.compute_preconditioner(b, mc.McConfig(rng_mode=rng))
+    want = oracle_mod.compute_preconditioner(b.n, b.row_ptr, b.col_idx, b.values, rng_mode=rng)
+    assert inv.stats["walk_steps"] == want.walk_steps
+    if rng == 0:
+        assert want.walk_steps == 2819436  # SURVEY.md §6 probe of the reference
+    assert inv.stats["walk_deg_sum"] == want.walk_deg_sum
+
+
+def test_identity_pipeline(mc):
+    # test_mc_engine.cpp:222-230
+    inv = mc.compute_preconditioner(mc.CsrMatrix.identity(6), mc.McConfig(alpha=1.0))
+    assert inv.m.nnz() == 6
+    assert all(inv.m.at(i, i) == 0.5 for i in range(6))
+    assert np.all(inv.row_meta.entries_before_retention == 1)
+    assert inv.budget_echo.n_chains >= 1
+
+
+def test_zero_variance_equals_truncated_neumann(mc):
+    # acceptance.cpp:124-162: one transition per P row -> deterministic walks
+    b = mc.CsrMatrix.from_triplets(6, list(range(6)) * 2, list(range(6)) + [1, 2, 3, 4, 5, 0],
+                                   [3.0, -3.0, 3.0, 3.0, -3.0, 3.0, 0.9, -0.8, 0.7, 0.6, 0.5, -0.4])
+    cfg = mc.McConfig(epsilon=0.1, delta=0.02, alpha=1.5)
+    ref = None
+    for seed in (0, 42, 987654321):
+        for rng in (0, 1):
+            cfg.master_seed, cfg.rng_mode = seed, rng
+            inv = mc.compute_preconditioner(b, cfg)
+            assert np.all(inv.row_meta.chains_used == 1)
+            if ref is None:
+                ref = inv.m
+            assert inv.m == ref
+
+
+def test_single_transition_chain_exact(mc):
+    # test_mc_engine.cpp:112-127 analogue at pipeline level: row 0 has one
+    # off-diagonal entry, so (I-A)^{-1} row 0 = [1, a] exactly for any seed
+    b = mc.CsrMatrix.from_triplets(2, [0, 0, 1], [0, 1, 1], [1.0, -0.5, 1.0])
+    for seed in (1, 99, 31337):
+        inv = mc.compute_preconditioner(b, mc.McConfig(alpha=1.0, master_seed=seed, delta=1e-6))
+        assert inv.row_meta.chains_used[0] == 1
+
+
+def test_empty_rows_missing_diagonal_and_n0(mc, ref_mod):
+    # structurally missing diagonal (split.cpp:10-42, test_mc_split.cpp:96-102)
+    b = mc.CsrMatrix.from_triplets(4, [0, 1, 3], [1, 0, 3], [0.5, 0.5, 2.0])
+    for rng in (0,):
+        inv = mc.compute_preconditioner(b, mc.McConfig(alpha=2.0))
+        want = ref_mod.compute_preconditioner(ref_mod.Csr(4, b.row_ptr, b.col_idx, b.values), alpha=2.0)
+        assert np.array_equal(inv.m.row_ptr, want.m.row_ptr)
+        assert np.array_equal(inv.m.col_idx, want.m.col_idx)
+        assert bits_equal(inv.m.values, want.m.values)
+    inv = mc.compute_preconditioner(mc.CsrMatrix(0, np.zeros(1, np.int64)), mc.McConfig())
+    assert inv.m.n == 0 and inv.m.nnz() == 0
+
+
+def test_errors_match_reference(mc):
+    two = mc.CsrMatrix.from_triplets(2, [0, 1], [0, 1], [-1.0, 1.0])
+    with pytest.raises(mc.SplitError, match="degenerate diagonal after augmentation at row 0"):
+        mc.compute_preconditioner(two, mc.McConfig(alpha=1.0, mode=mc.AugmentationMode.plain))
+    dom = mc.CsrMatrix.from_triplets(2, [0, 0, 1], [0, 1, 1], [-10.0, 10.0, 1.0])
+    with pytest.raises(mc.SplitError, match="diagonal dominance failure"):
+        mc.compute_preconditioner(dom, mc.McConfig(alpha=1.0, mode=mc.AugmentationMode.plain))
+    with pytest.raises(ValueError, match="drop fraction"):
+        mc.compute_preconditioner(two, mc.McConfig(drop_fraction=1.5))
+    with pytest.raises(ValueError, match="alpha must be positive"):
+        mc.compute_preconditioner(two, mc.McConfig(alpha=0.0))
+    bad = mc.CsrMatrix(2, np.array([0, 1, 2]), np.array([0, 7]), np.array([1.0, 1.0]))
+    with pytest.raises(IndexError):
+        mc.compute_preconditioner(bad, mc.McConfig())
+
+
+def test_determinism_repeat(mc):
+    b = _csr(mc, "brusselator:32")
+    cfg = mc.McConfig(epsilon=.05, delta=.01, alpha=1.5, retain_k=32, master_seed=20260826)
+    a = mc.compute_preconditioner(b, cfg)
+    c = mc.compute_preconditioner(b, cfg)
+    assert a.m == c.m
+
+
+def test_row_shards_concatenate_to_full(mc):
+    import torch
+    from paper_2409_03095_b200.engine import DeviceEngine
+    b = _csr(mc, "convdiff:64:20:10")
+    eng = DeviceEngine(0)
+    rp, ci, v = DeviceEngine.upload(b)
+    for rng in (0, 1):
+        cfg = mc.McConfig(master_seed=7, rng_mode=rng)
+        full = eng.to_tensors(eng.build(b.n, rp, ci, v, cfg))
+        parts = []
+        for lo, hi in ((0, 1000), (1000, 1001), (1001, 2500), (2500, 4096)):
+            parts.append(eng.to_tensors(eng.build(b.n, rp, ci, v, cfg, lo, hi)))
+        cols = torch.cat([p[1] for p in parts])
+        vals = torch.cat([p[2] for p in parts])
+        assert torch.equal(cols, full[1]) and torch.equal(vals.view(torch.int64), full[2].view(torch.int64))
+        off = 0
+        rps = []
+        for p in parts:
+            rps.append(p[0][:-1] + off)
+            off += int(p[0][-1])
+        assert torch.equal(torch.cat(rps + [torch.tensor([off], device=rp.device)]), full[0])
+    eng.close()
+
+
+@pytest.mark.parametrize("rng", [0, 1])
+def test_overflow_tier_retry(mc, oracle_mod, rng):
+    # long walks on a dense-ish random matrix force rows past the first
+    # accumulator tier; the retried rows must still be exact
+    b = _csr(mc, "broad:1024:24:1e-4:1:7")
+    cfg = mc.McConfig(epsilon=.02, delta=.01, alpha=1.5, master_seed=42, rng_mode=rng)
+    inv = mc.compute_preconditioner(b, cfg)
+    assert inv.stats["rows_retried"] > 0
+    want = oracle_mod.compute_preconditioner(b.n, b.row_ptr, b.col_idx, b.values, **cfg.oracle_kwargs())
+    assert bits_equal(inv.m.values, want.values) and np.array_equal(inv.m.col_idx, want.col_idx)
+
+
+def test_keyed_within_mc_tolerance_of_reference(mc):
+    import scipy.sparse as sp
+    from paper_2409_03095_b200 import generators as G
+    for b, cfg in ((G.convection_diffusion(100, 0.0, 0.0), mc.McConfig()),
+                   (G.convection_diffusion(64), mc.McConfig(master_seed=7)),
+                   (G.convection_diffusion(40, 0.0, 0.0), mc.McConfig(epsilon=.01, delta=.01))):
+        cfg.rng_mode = mc.RngMode.reference
+        r = mc.compute_preconditioner(b, cfg)
+        cfg.rng_mode = mc.RngMode.keyed
+        k = mc.compute_preconditioner(b, cfg)
+        n = b.n
+        MR = sp.csr_matrix((r.m.values, r.m.col_idx, r.m.row_ptr), shape=(n, n))
+        MK = sp.csr_matrix((k.m.values, k.m.col_idx, k.m.row_ptr), shape=(n, n))
+        B = sp.csr_matrix((b.values, b.col_idx, b.row_ptr), shape=(n, n))
+        shift = cfg.alpha * abs(B).sum(axis=1).max()
+        Bh = B + sp.diags(np.where(B.diagonal() < 0, -shift, shift))
+        eps = cfg.epsilon
+        d = MK - MR
+        assert sp.linalg.norm(d) / sp.linalg.norm(MR) <= 0.3 * eps
+        assert abs(d).max() <= 0.5 * eps * abs(MR).max()
+        I = sp.identity(n)
+        fr = lambda M: sp.linalg.norm(I - Bh @ M) / np.sqrt(n)  # noqa: E731
+        assert abs(fr(MK) - fr(MR)) <= 0.1 * fr(MR)
+
+
+@pytest.mark.slow
+@pytest.mark.parametrize("cfgname", ["c3_lap3d_100", "c2_sym27_1p3m", "c4_convdiff_1000", "c3_lap3d_100_heavy"])
+@pytest.mark.parametrize("rng", [0, 1])
+def test_full_size_row_windows_bit_identical(mc, oracle_mod, cfgname, rng):
+    from paper_2409_03095_b200 import generators as G
+    gen, over = G.CONFIGS[cfgname]
+    b = gen()
+    cfg = mc.McConfig(rng_mode=rng, **over)
+    inv = mc.compute_preconditioner(b, cfg)
+    assert inv.m.row_ptr[-1] == inv.m.nnz()
+    n = b.n
+    windows = [(0, 64), (n // 2, n // 2 + 64), (n - 64, n)]
+    for lo, hi in windows:
+        want = oracle_mod.compute_preconditioner(n, b.row_ptr, b.col_idx, b.values, row_begin=lo, row_end=hi,
+                                                 **cfg.oracle_kwargs())
+        a, z = inv.m.row_ptr[lo], inv.m.row_ptr[hi]
+        assert np.array_equal(inv.m.row_ptr[lo:hi + 1] - a, want.row_ptr)
+        assert np.array_equal(inv.m.col_idx[a:z], want.col_idx)
+        assert bits_equal(inv.m.values[a:z], want.values)
+        assert np.array_equal(inv.row_meta.chains_used[lo:hi], want.chains_used)
+        assert np.array_equal(inv.row_meta.entries_before_retention[lo:hi], want.entries_before)
+    # size-independent properties at full size
+    assert np.all(np.diff(inv.m.row_ptr) >= 1)  # diagonal always kept
+    rows = np.repeat(np.arange(n), np.diff(inv.m.row_ptr))
+    assert np.all(inv.m.values[inv.m.col_idx == rows] != 0.0)
+    assert inv.stats["rows_retried"] >= 0
