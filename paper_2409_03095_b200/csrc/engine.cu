@@ -150,7 +150,7 @@ struct mcmi_engine {
     int num_sms = 148;
     cudaStream_t own = nullptr;
     cudaEvent_t ev[6] = {};
-    DevBuf red, diag_val, a_cnt, a_off, keep, desc, ent, colA, b1, scan_tmp, cq_tmp;
+    DevBuf red, diag_val, a_cnt, a_off, keep, rec, ent, colA, b1, scan_tmp, cq_tmp;
     DevBuf stage_col, stage_val, row_cnt, row_src, chains_used, entries_before, counters;
     DevBuf ovf[2];
     DevBuf out_rp, out_col, out_val;
@@ -185,7 +185,7 @@ Status engine_init(mcmi_engine* e, int device) {
 
 void engine_release(mcmi_engine* e) {
     cudaSetDevice(e->device);
-    for (DevBuf* b : {&e->red, &e->diag_val, &e->a_cnt, &e->a_off, &e->keep, &e->desc, &e->ent,
+    for (DevBuf* b : {&e->red, &e->diag_val, &e->a_cnt, &e->a_off, &e->keep, &e->rec, &e->ent,
                       &e->colA, &e->b1, &e->scan_tmp, &e->cq_tmp, &e->stage_col, &e->stage_val,
                       &e->row_cnt, &e->row_src, &e->chains_used, &e->entries_before,
                       &e->counters, &e->ovf[0], &e->ovf[1], &e->out_rp, &e->out_col,
@@ -209,7 +209,7 @@ Tier make_tier(int cap, int64_t max_len) {
     Tier t;
     t.cap = cap;
     t.cap_limit = cap - cap / 4;
-    const int64_t s64 = std::max<int64_t>(1, max_len) + 1;
+    const int64_t s64 = std::max<int64_t>(1, max_len);
     t.log_stride = static_cast<int>(std::min<int64_t>(s64, INT_MAX / 64));
     const int logmax = std::max(kLogMax, t.log_stride);
     t.lanes = std::max(1, std::min(32, logmax / t.log_stride));
@@ -255,7 +255,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     MCMI_TRY(e->diag_val.ensure(n1 * sizeof(double)), "alloc diag");
     MCMI_TRY(e->a_cnt.ensure(n1 * sizeof(unsigned)), "alloc a_cnt");
     MCMI_TRY(e->a_off.ensure((n1 + 1) * sizeof(unsigned)), "alloc a_off");
-    MCMI_TRY(e->desc.ensure(n1 * sizeof(uint2)), "alloc desc");
+    MCMI_TRY(e->rec.ensure(2 * n1 * sizeof(uint4)), "alloc rec");
     MCMI_TRY(e->ent.ensure(z1 * sizeof(double2)), "alloc ent");
     MCMI_TRY(e->colA.ensure(z1 * sizeof(int)), "alloc col");
     MCMI_TRY(e->b1.ensure(n1 * sizeof(double)), "alloc b1");
@@ -283,7 +283,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     ta.a_cnt = e->a_cnt.as<unsigned>();
     ta.a_off = e->a_off.as<unsigned>();
     ta.keep = nullptr;
-    ta.desc = e->desc.as<uint2>();
+    ta.rec = e->rec.as<uint4>();
     ta.ent = e->ent.as<double2>();
     ta.col = e->colA.as<int>();
     ta.b1_diag = e->b1.as<double>();
@@ -371,7 +371,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
                  "alloc staging");
         MCMI_TRY(cudaMemsetAsync(e->counters.p, 0, 8 * sizeof(unsigned long long), s), "memset");
         WalkArgs wa{};
-        wa.t = Tables{n, e->desc.as<uint2>(), e->ent.as<double2>(), e->colA.as<int>(), e->b1.as<double>()};
+        wa.t = Tables{n, e->rec.as<uint4>(), e->ent.as<double2>(), e->colA.as<int>(), e->b1.as<double>()};
         wa.row_begin = row_begin;
         wa.row_list = row_list;
         wa.n_work = work;
@@ -385,6 +385,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         wa.cap_limit = t.cap_limit;
         wa.lanes = t.lanes;
         wa.log_stride = t.log_stride;
+        wa.log_magic = static_cast<unsigned>((0x100000000ull + t.log_stride - 1) / t.log_stride);
         wa.ell0 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(L, 2)));
         wa.stage_col = e->stage_col.as<int>();
         wa.stage_val = e->stage_val.as<double>();

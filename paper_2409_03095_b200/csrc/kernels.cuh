@@ -21,14 +21,21 @@ struct Reductions {
     unsigned long long pad[6];
 };
 
-// Transition tables (subsystem 1), one record per state s of the walk:
-//   desc[s] = {begin, deg} into the entry arrays (A's row s)
+// Transition tables (subsystem 1), one 32-byte record per state s:
+//   rec[2s]   = {begin, deg, guide[0..3], guide[4..7]}
+//   rec[2s+1] = {guide[8..11], guide[12..15], col (deg==1), 0}
+//   deg == 1 : rec[2s].zw holds the forced move's ratio (f64) instead of guide[0..7]
+//   guide[m] (u8, in units of ceil(deg/255)) = first k with cum_k > m/16, so the
+//   inverse-CDF scan for u starts at guide[floor(16u)] and returns the same k as
+//   the reference's full scan (all skipped cum_k <= m/16 <= u).
 //   ent[k]  = {cum_k, ratio_k}: running sequential sum of p (sample_transition's
 //             `cum`, mc_engine.cpp:71-75) and a_k / p_k (mc_engine.cpp:94)
 //   col[k]  = column of A (int32)
+constexpr int kGuide = 16;
+
 struct Tables {
     int64_t n;
-    const uint2* desc;
+    const uint4* rec;
     const double2* ent;
     const int* col;
     const double* b1_diag;  // diag(B_hat) = B1 (split.cpp:70)
@@ -49,7 +56,7 @@ struct TableBuildArgs {
     unsigned* a_cnt;      // [n]
     unsigned* a_off;      // [n+1]
     unsigned char* keep;  // [nnz] count-quantile keep flags (or nullptr)
-    uint2* desc;
+    uint4* rec;           // [2n]
     double2* ent;
     int* col;
     double* b1_diag;
@@ -69,7 +76,8 @@ struct WalkArgs {
     int cap;                // hash capacity (power of two)
     int cap_limit;          // max distinct columns before the row overflows to the next tier
     int lanes;              // chains per batch (<= 32)
-    int log_stride;         // max_len + 1 deposits per chain
+    int log_stride;         // max(max_len, 1) step deposits per chain
+    unsigned log_magic;     // ceil(2^32 / log_stride): p / log_stride == __umulhi(p, log_magic)
     int ell0;               // initial speculative draw stride (reference-stream mode)
     // outputs, indexed by local row (row - row_begin)
     int* stage_col;

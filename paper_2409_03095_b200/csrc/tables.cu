@@ -15,12 +15,14 @@
 // -fmad=false every value here is bit-identical to the reference's.
 //
 // HBM layout produced (B200, 180 GB):
-//   desc[n]     uint2  {begin, deg}           8 B per state
+//   rec[n]      2 x uint4 {begin, deg, guide[16], inline forced move}
+//                                            32 B per state (one sector)
 //   ent[nnz_A]  double2 {cum, a/p}           16 B per transition
 //   col[nnz_A]  int32                         4 B per transition
 //   b1_diag[n]  f64                           8 B per state
-// A step from state s reads desc[s] (1 sector), ent[begin .. k] (sequential)
-// and col[k]: the 20 + 8*deg(s) algorithmic bytes of SURVEY.md §8(d).
+// A step from state s reads rec[s] (1 sector), ent[begin+guide .. k] (usually
+// 1 sector) and col[k]; SURVEY.md §8(d) counts 20 + 8*deg(s) algorithmic bytes
+// (the full CDF row), which the guide avoids re-reading.
 #include <climits>
 
 #include "common.cuh"
@@ -160,7 +162,8 @@ __global__ void k_rows_split(TableBuildArgs a) {
 }
 
 // Pass D: transition records (split.cpp:75-92 values, split.cpp:102-119
-// probabilities, mc_engine.cpp:71-75 running CDF, mc_engine.cpp:94 ratio).
+// probabilities, mc_engine.cpp:71-75 running CDF, mc_engine.cpp:94 ratio)
+// plus the 16-bucket guide of each state's CDF.
 __global__ void k_rows_fill(TableBuildArgs a) {
     const Keep keep = make_keep(a);
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
@@ -168,32 +171,59 @@ __global__ void k_rows_fill(TableBuildArgs a) {
         const double b1 = a.b1_diag[i];
         const unsigned begin = a.a_off[i];
         const unsigned cnt = a.a_cnt[i];
-        a.desc[i] = make_uint2(begin, cnt);
-        if (cnt == 0) continue;
-        const int64_t k0 = a.row_ptr[i], k1 = a.row_ptr[i + 1];
-        double row_sum = 0.0;  // transition_probabilities' sum == split's row_sum
-        for (int64_t k = k0; k < k1; ++k) {
-            const int64_t c = a.col_idx[k];
-            const double v = a.values[k];
-            if (c == i || c < 0 || c >= a.n || !keep(i, k, c, v)) continue;
-            const double av = -v / b1;
-            if (av == 0.0) continue;
-            row_sum += fabs(av);
+        uint4 r0 = make_uint4(begin, cnt, 0u, 0u), r1 = make_uint4(0u, 0u, 0u, 0u);
+        if (cnt > 0) {
+            const int64_t k0 = a.row_ptr[i], k1 = a.row_ptr[i + 1];
+            double row_sum = 0.0;  // transition_probabilities' sum == split's row_sum
+            for (int64_t k = k0; k < k1; ++k) {
+                const int64_t c = a.col_idx[k];
+                const double v = a.values[k];
+                if (c == i || c < 0 || c >= a.n || !keep(i, k, c, v)) continue;
+                const double av = -v / b1;
+                if (av == 0.0) continue;
+                row_sum += fabs(av);
+            }
+            const unsigned scale = (cnt + 254u) / 255u;
+            unsigned char g[kGuide];
+            int m_next = 0;
+            double cum = 0.0;
+            unsigned o = 0;
+            for (int64_t k = k0; k < k1; ++k) {
+                const int64_t c = a.col_idx[k];
+                const double v = a.values[k];
+                if (c == i || c < 0 || c >= a.n || !keep(i, k, c, v)) continue;
+                const double av = -v / b1;
+                if (av == 0.0) continue;
+                const double p = fabs(av) / row_sum;
+                cum += p;
+                const double ratio = av / p;
+                a.ent[begin + o] = make_double2(cum, ratio);
+                a.col[begin + o] = static_cast<int>(c);
+                if (cnt == 1) {
+                    const unsigned long long rb = static_cast<unsigned long long>(__double_as_longlong(ratio));
+                    r0.z = static_cast<unsigned>(rb);
+                    r0.w = static_cast<unsigned>(rb >> 32);
+                    r1.z = static_cast<unsigned>(c);
+                }
+                // guide: first o with cum_o > m/16 (m/16 exact in binary)
+                while (m_next < kGuide && cum > static_cast<double>(m_next) * (1.0 / kGuide))
+                    g[m_next++] = static_cast<unsigned char>(o / scale);
+                ++o;
+            }
+            while (m_next < kGuide) g[m_next++] = static_cast<unsigned char>(cnt / scale);
+            if (cnt >= 2) {
+                unsigned w[4];
+                for (int q = 0; q < 4; ++q)
+                    w[q] = g[4 * q] | (g[4 * q + 1] << 8) | (g[4 * q + 2] << 16) |
+                           (static_cast<unsigned>(g[4 * q + 3]) << 24);
+                r0.z = w[0];
+                r0.w = w[1];
+                r1.x = w[2];
+                r1.y = w[3];
+            }
         }
-        double cum = 0.0;
-        unsigned o = begin;
-        for (int64_t k = k0; k < k1; ++k) {
-            const int64_t c = a.col_idx[k];
-            const double v = a.values[k];
-            if (c == i || c < 0 || c >= a.n || !keep(i, k, c, v)) continue;
-            const double av = -v / b1;
-            if (av == 0.0) continue;
-            const double p = fabs(av) / row_sum;
-            cum += p;
-            a.ent[o] = make_double2(cum, av / p);
-            a.col[o] = static_cast<int>(c);
-            ++o;
-        }
+        a.rec[2 * i] = r0;
+        a.rec[2 * i + 1] = r1;
     }
 }
 

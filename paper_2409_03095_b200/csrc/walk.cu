@@ -84,6 +84,20 @@ __device__ __forceinline__ int hash_slot(int* keys, unsigned mask, int shift, in
     return -1;
 }
 
+// acc += 1.0, k times, with the rounding of k sequential additions.  When
+// acc >= 1 and acc + k stays in acc's binade, every intermediate sum is a
+// representable integer multiple of ulp(acc), so one addition is exact; a
+// binade crossing (~log2(N) times per row) takes the sequential path.
+__device__ __forceinline__ double add_ones(double acc, int k) {
+    if (k <= 0) return acc;
+    if (acc >= 1.0 && acc < 0x1.0p53) {
+        const double t = acc + static_cast<double>(k);
+        if ((__double_as_longlong(t) >> 52) == (__double_as_longlong(acc) >> 52)) return t;
+    }
+    for (; k > 0; --k) acc += 1.0;
+    return acc;
+}
+
 __device__ __forceinline__ int warp_sum_int(int v) {
 #pragma unroll
     for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
@@ -111,7 +125,7 @@ __global__ void __launch_bounds__(256) k_walk(const WalkArgs a) {
     const int lane = static_cast<int>(threadIdx.x & 31);
     const int warp = static_cast<int>(threadIdx.x >> 5);
     const int cap = a.cap;
-    const int S = a.log_stride;                 // deposits per chain: W0 + max_len
+    const int S = a.log_stride;                 // step deposits per chain (max_len)
     const int B = a.lanes;                      // chains per batch
     const int logn = round32(B * S);
     const size_t per_warp = static_cast<size_t>(cap + logn) * 12;
@@ -120,7 +134,7 @@ __global__ void __launch_bounds__(256) k_walk(const WalkArgs a) {
     const int shift = 32 - (31 - __clz(cap));
     const unsigned lt_mask = (1u << lane) - 1u;
 
-    const uint2* __restrict__ desc = a.t.desc;
+    const uint4* __restrict__ rec = a.t.rec;
     const double2* __restrict__ ent = a.t.ent;
     const int* __restrict__ tcol = a.t.col;
     const uint2 key = make_uint2(static_cast<uint32_t>(a.seed), static_cast<uint32_t>(a.seed >> 32));
@@ -142,15 +156,21 @@ __global__ void __launch_bounds__(256) k_walk(const WalkArgs a) {
             sm.vals[i] = 0.0;
         }
         __syncwarp();
+        // the diagonal column's slot; its sum lives in a register (acc_r)
+        int n_new0 = 0;
+        int slot_r = 0;
+        if (lane == 0) slot_r = hash_slot(sm.keys, cap_mask, shift, rowc, n_new0);
+        slot_r = __shfl_sync(FULL_MASK, slot_r, 0);
+        double acc_r = 0.0;
 
-        int distinct = 0;
+        int distinct = 1;
         bool overflow = false;
         int64_t chains_done = 0;
         int64_t chains_run = N;
         unsigned long long row_steps = 0, row_deg = 0;
         // reference-stream speculation state
         unsigned long long D = 0;
-        unsigned long long ell = static_cast<unsigned long long>(a.ell0);
+        unsigned ell = static_cast<unsigned>(a.ell0);
         bool row_done = false;
 
         while (!row_done) {
@@ -167,34 +187,34 @@ __global__ void __launch_bounds__(256) k_walk(const WalkArgs a) {
             }
             int* lc = sm.log_col + lane * S;
             double* lw = sm.log_w + lane * S;
-            int m = 0;
-            if (active) {
-                lc[0] = rowc;  // W0 = 1 lands on (r, r) (mc_engine.cpp:89)
-                lw[0] = 1.0;
-                m = 1;
-            }
+            int m = 0;              // step deposits logged (W0 = 1 at (r, r) is implicit)
+            unsigned retm = 0;      // bit t: step deposit t went back to column r (t < 32)
+            bool ret_hi = false;    // a return at t >= 32
             int state = rowc;
             double w = 1.0;
-            unsigned long long draws = 0;
+            unsigned draws = 0;
+            unsigned lane_steps = 0, lane_deg = 0;  // committed only if this lane's chain counts
             unsigned long long cached = ~0ull;
             uint4 blk = make_uint4(0, 0, 0, 0);
             bool alive = active;
             for (int64_t t = 0; __any_sync(FULL_MASK, alive); ++t) {
                 if (alive && t >= L) alive = false;
                 if (!alive) continue;
-                const uint2 d = desc[state];
-                if (d.y == 0) {  // absorbing state (mc_engine.cpp:68)
+                const uint4 r0 = rec[2 * static_cast<int64_t>(state)];
+                const unsigned deg = r0.y;
+                if (deg == 0) {  // absorbing state (mc_engine.cpp:68)
                     alive = false;
                     continue;
                 }
-                ++row_steps;
-                row_deg += d.y;
-                unsigned k;
+                ++lane_steps;
+                lane_deg += deg;
                 double ratio;
-                if (d.y == 1) {  // forced move, no draw (mc_engine.cpp:69)
-                    k = d.x;
-                    ratio = ent[k].y;
+                int nxt;
+                if (deg == 1) {  // forced move, no draw (mc_engine.cpp:69); inline in the record
+                    ratio = __hiloint2double(static_cast<int>(r0.w), static_cast<int>(r0.z));
+                    nxt = static_cast<int>(rec[2 * static_cast<int64_t>(state) + 1].z);
                 } else {
+                    const uint4 r1 = rec[2 * static_cast<int64_t>(state) + 1];
                     double u;
                     if (MODE == 0) {
                         const unsigned long long b = pos >> 1;
@@ -223,32 +243,55 @@ __global__ void __launch_bounds__(256) k_walk(const WalkArgs a) {
                                     : u32pair_to_double(blk.x, blk.y);
                     }
                     ++draws;
-                    // inverse CDF: first k with u < cum_k, else the last entry
-                    // (mc_engine.cpp:71-77)
-                    const unsigned end = d.x + d.y;
-                    k = end - 1;
+                    // inverse CDF (mc_engine.cpp:71-77): first k with u < cum_k, else
+                    // the last entry.  Start at the guide bucket of u: every skipped
+                    // entry has cum <= m/16 <= u.
+                    const int mb = static_cast<int>(u * static_cast<double>(kGuide));
+                    const unsigned gw = mb < 8 ? (mb < 4 ? r0.z : r0.w) : (mb < 12 ? r1.x : r1.y);
+                    const unsigned g = (gw >> ((mb & 3) * 8)) & 0xffu;
+                    const unsigned end = r0.x + deg;
+                    unsigned q = r0.x + g * ((deg + 254u) / 255u);
+                    unsigned k = end - 1;
+                    bool found = false;
                     ratio = 0.0;
-                    for (unsigned q = d.x; q < end; ++q) {
-                        const double2 e = ent[q];
-                        ratio = e.y;
-                        if (u < e.x) {
+                    for (; q < end; q += 2) {
+                        const double2 e0 = ent[q];
+                        const double2 e1 = ent[min(q + 1, end - 1)];
+                        if (u < e0.x) {
                             k = q;
+                            ratio = e0.y;
+                            found = true;
+                            break;
+                        }
+                        if (u < e1.x) {
+                            k = min(q + 1, end - 1);
+                            ratio = e1.y;
+                            found = true;
                             break;
                         }
                     }
+                    if (!found) ratio = ent[end - 1].y;
+                    nxt = tcol[k];
                 }
                 w *= ratio;  // w *= a_k / p_k (mc_engine.cpp:94)
-                state = tcol[k];
+                state = nxt;
                 lc[m] = state;
                 lw[m] = w;
                 ++m;
+                if (state == rowc) {
+                    if (m <= 32) retm |= 1u << (m - 1);
+                    else ret_hi = true;
+                }
                 if (fabs(w) < a.delta) alive = false;  // mc_engine.cpp:97
             }
+
+            if (active)
+                for (int t1 = m; t1 < S; ++t1) lc[t1] = -1;  // end-of-chain sentinel for the fold
 
             // ------------------------------------------- which lanes count
             unsigned valid;
             const bool first = chains_done == 0;
-            const unsigned long long draws0 = __shfl_sync(FULL_MASK, draws, 0);
+            const unsigned draws0 = __shfl_sync(FULL_MASK, draws, 0);
             if (first && draws0 == 0) {
                 // chain 0 consumed no randomness: its single realization is the
                 // estimator mean (mc_engine.cpp:101-104)
@@ -256,14 +299,14 @@ __global__ void __launch_bounds__(256) k_walk(const WalkArgs a) {
                 chains_run = 1;
                 row_done = true;
             } else if (MODE == 0) {
-                int nxt = lane;
-                if (active && draws > 0 && draws % ell == 0) {
-                    const unsigned long long q = draws / ell;
-                    if (static_cast<unsigned long long>(lane) + q < static_cast<unsigned long long>(B))
-                        nxt = lane + static_cast<int>(q);
+                int nxtl = lane;
+                if (active && draws > 0) {
+                    const unsigned q = draws / ell;
+                    if (q * ell == draws && static_cast<unsigned>(lane) + q < static_cast<unsigned>(B))
+                        nxtl = lane + static_cast<int>(q);
                 }
-                unsigned R = (1u << lane) | (1u << nxt);
-                int J = nxt;
+                unsigned R = (1u << lane) | (1u << nxtl);
+                int J = nxtl;
 #pragma unroll
                 for (int i = 0; i < 5; ++i) {
                     const unsigned Rn = __shfl_sync(FULL_MASK, R, J);
@@ -278,26 +321,57 @@ __global__ void __launch_bounds__(256) k_walk(const WalkArgs a) {
             const int64_t remaining = N - chains_done;
             while (static_cast<int64_t>(__popc(valid)) > remaining)
                 valid &= ~(1u << (31 - __clz(valid)));
+            const bool mine = (valid >> lane) & 1u;
+            if (mine) {
+                row_steps += lane_steps;
+                row_deg += lane_deg;
+            }
             if (MODE == 0 && !row_done) {
                 const int lv = 31 - __clz(valid);
-                const unsigned long long klv = __shfl_sync(FULL_MASK, draws, lv);
+                const unsigned klv = __shfl_sync(FULL_MASK, draws, lv);
                 D = D + static_cast<unsigned long long>(lv) * ell + klv;
-                ell = draws0 > 0 ? draws0 : 1ull;
+                ell = draws0 > 0 ? draws0 : 1u;
             }
             __syncwarp();
 
             // ------------------------------------- ordered (chain, step) fold
+            // (i) column r: W0 = +1.0 per valid chain plus its returns, in
+            // chain order, folded in a register (warp-uniform).
+            {
+                unsigned rl = __ballot_sync(FULL_MASK, mine && (retm != 0 || ret_hi));
+                unsigned done_mask = 0;  // lanes already folded
+                while (rl) {
+                    const int j = __ffs(rl) - 1;
+                    rl &= rl - 1;
+                    acc_r = add_ones(acc_r, __popc(valid & ((1u << j) - 1u) & ~done_mask) + 1);
+                    unsigned rm = __shfl_sync(FULL_MASK, retm, j);
+                    const bool hi = __shfl_sync(FULL_MASK, static_cast<int>(ret_hi), j) != 0;
+                    while (rm) {
+                        const int t1 = __ffs(rm) - 1;
+                        rm &= rm - 1;
+                        acc_r += sm.log_w[j * S + t1];
+                    }
+                    if (hi) {
+                        const int mj = __shfl_sync(FULL_MASK, m, j);
+                        for (int t1 = 32; t1 < mj; ++t1)
+                            if (sm.log_col[j * S + t1] == rowc) acc_r += sm.log_w[j * S + t1];
+                    }
+                    done_mask = (j == 31) ? FULL_MASK : ((1u << (j + 1)) - 1u);
+                }
+                acc_r = add_ones(acc_r, __popc(valid & ~done_mask));
+            }
+            // (ii) every other column: 32-position chunks of the chain-major log;
+            // equal columns grouped by __match_any_sync, leader adds in lane order.
             int n_new = 0;
             bool fail = false;
             const int span = B * S;
             for (int base = 0; base < span; base += 32) {
                 const int p = base + lane;
-                int c = -1 - lane;  // unique non-column tag for empty positions
-                const int j = min(p / S, 31);
-                const int tt = p - j * S;
-                const int mj = __shfl_sync(FULL_MASK, m, j);
-                const bool ok = p < span && ((valid >> j) & 1u) && tt < mj;
-                if (ok) c = sm.log_col[p];
+                const int j = min(static_cast<int>(__umulhi(static_cast<unsigned>(p), a.log_magic)), 31);
+                bool ok = p < span && ((valid >> j) & 1u);
+                int c = ok ? sm.log_col[p] : -1;
+                ok = ok && c >= 0 && c != rowc;  // column r was folded in (i)
+                if (!ok) c = -1 - lane;          // unique non-column tag
                 const unsigned peers = __match_any_sync(FULL_MASK, c);
                 if (ok && (__ffs(peers) - 1) == lane) {
                     const int slot = hash_slot(sm.keys, cap_mask, shift, c, n_new);
@@ -335,6 +409,8 @@ __global__ void __launch_bounds__(256) k_walk(const WalkArgs a) {
         }
         tot_steps += row_steps;
         tot_deg += row_deg;
+        if (lane == 0) sm.vals[slot_r] = acc_r;
+        __syncwarp();
 
         // ------------------------------------------------------ finalize
         // compact occupied slots to [0, distinct) (in place, order-preserving)

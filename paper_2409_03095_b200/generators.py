@@ -169,6 +169,7 @@ def powerlaw(n: int, gamma: float = 2.1, dmin: int = 2, dmax: int = 2000, seed: 
 CONFIGS = {
     "c1_poisson2d_100": (lambda: convection_diffusion(100, 0.0, 0.0), {}),
     "c2_sym27_1p3m": (lambda: stencil27(), {"epsilon": 0.01, "delta": 0.01}),
+    "c2_sym27_default": (lambda: stencil27(), {}),
     "c3_lap3d_100": (lambda: laplacian3d(100), {}),
     "c3_lap3d_100_heavy": (lambda: laplacian3d(100), {"epsilon": 0.01, "delta": 0.01, "alpha": 1.5}),
     "c4_convdiff_1000": (lambda: convection_diffusion(1000), {}),
