@@ -210,38 +210,6 @@ def run_reference_arm(args):
 
 # ------------------------------------------------------------------ our arm
 
-def allgatherv_csr(rp, ci, v, dist, device):
-    """NCCL all-gather of variable-size CSR shards into the full M on every rank."""
-    import torch
-    world = dist.get_world_size()
-    nnz = torch.tensor([ci.numel(), rp.numel() - 1], dtype=torch.int64, device=device)
-    sizes = [torch.empty_like(nnz) for _ in range(world)]
-    dist.all_gather(sizes, nnz)
-    sizes = torch.stack(sizes).cpu()
-    mx, mr = int(sizes[:, 0].max()), int(sizes[:, 1].max())
-    pad_c = torch.zeros(max(mx, 1), dtype=torch.int64, device=device)
-    pad_v = torch.zeros(max(mx, 1), dtype=torch.float64, device=device)
-    pad_r = torch.zeros(mr + 1, dtype=torch.int64, device=device)
-    pad_c[: ci.numel()] = ci
-    pad_v[: v.numel()] = v
-    pad_r[: rp.numel()] = rp
-    gc = torch.empty(world * pad_c.numel(), dtype=torch.int64, device=device)
-    gv = torch.empty(world * pad_v.numel(), dtype=torch.float64, device=device)
-    gr = torch.empty(world * pad_r.numel(), dtype=torch.int64, device=device)
-    dist.all_gather_into_tensor(gc, pad_c)
-    dist.all_gather_into_tensor(gv, pad_v)
-    dist.all_gather_into_tensor(gr, pad_r)
-    cols, vals, rps, off = [], [], [], 0
-    for g in range(world):
-        k, r = int(sizes[g, 0]), int(sizes[g, 1])
-        cols.append(gc[g * pad_c.numel(): g * pad_c.numel() + k])
-        vals.append(gv[g * pad_v.numel(): g * pad_v.numel() + k])
-        rps.append(gr[g * pad_r.numel(): g * pad_r.numel() + r] + off)
-        off += k
-    rps.append(torch.tensor([off], dtype=torch.int64, device=device))
-    return torch.cat(rps), torch.cat(cols), torch.cat(vals)
-
-
 def load_traffic(workload, rng):
     path = os.path.join(REPO, "profiles", "walk_traffic.json")
     try:
@@ -265,14 +233,14 @@ def run_ours(args):
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
 
+    from paper_2409_03095_b200.distributed import allgatherv_csr, partition_rows
     from paper_2409_03095_b200.engine import DeviceEngine
     from paper_2409_03095_b200.mcspai import RngMode, compute_preconditioner
 
     b, cfg = make_workload(args.config)
     cfg.rng_mode = RngMode.reference if args.rng == "reference" else RngMode.keyed
     cfg.device = local
-    lo = b.n * rank // world
-    hi = b.n * (rank + 1) // world
+    lo, hi = partition_rows(b.row_ptr, world)[rank]
     eng = DeviceEngine(local)
     d_rp, d_ci, d_v = DeviceEngine.upload(b, local)
     stream = torch.cuda.current_stream(device)
@@ -281,7 +249,7 @@ def run_ours(args):
         d = eng.build(b.n, d_rp, d_ci, d_v, cfg, lo, hi, stream=stream)
         if world > 1:
             rp, ci, v, _, _ = eng.to_tensors(d, stream=stream)
-            allgatherv_csr(rp, ci, v, dist, device)
+            allgatherv_csr(rp, ci, v, dist)
         return d
 
     for _ in range(max(args.warmup, 0)):

@@ -1,0 +1,114 @@
+// include/mcmi/mcspai_compat.hpp — header-only C++ drop-in over the C-ABI.
+//
+// Replaces the body of
+//   mcspai::compute_preconditioner(const CsrMatrix&, const McConfig&, int)
+//   (/root/reference/proj/include/mcspai/mc_engine.hpp:80-81,
+//    /root/reference/proj/src/mc_engine.cpp:230-233)
+// with the B200 build, operating directly on the reference's own types:
+//
+//   #include "mcmi/mcspai_compat.hpp"
+//   ApproxInverse compute_preconditioner(const CsrMatrix& b, const McConfig& cfg, int) {
+//       return mcmi::compat::compute_preconditioner<ApproxInverse, SplitError>(b, cfg);
+//   }
+//
+// The templates only touch the fields the reference declares:
+//   CsrMatrix      n, row_ptr, col_idx, values          (csr.hpp:16-21)
+//   McConfig       epsilon .. master_seed                (mc_engine.hpp:15-26)
+//   ApproxInverse  m, row_meta, config_echo, budget_echo, seed_echo (mc_engine.hpp:39-45)
+// Errors are re-thrown as the reference throws them: std::invalid_argument
+// (csr.cpp:129, split.cpp:48, mc_engine.cpp:14), SplitErrorT (split.cpp:68,95),
+// std::out_of_range (bad column index), std::runtime_error (CUDA / device).
+#ifndef MCMI_MCSPAI_COMPAT_HPP
+#define MCMI_MCSPAI_COMPAT_HPP
+
+#include <cstdint>
+#include <new>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../mcmi.h"
+
+namespace mcmi {
+namespace compat {
+
+struct Options {
+    int device = 0;                      // CUDA device ordinal
+    int rng_mode = MCMI_RNG_REFERENCE;   // byte-identical to the reference by default
+};
+
+template <class CfgT>
+mcmi_config to_config(const CfgT& cfg, const Options& opt) {
+    mcmi_config c;
+    mcmi_config_default(&c);
+    c.epsilon = cfg.epsilon;
+    c.delta = cfg.delta;
+    c.alpha = cfg.alpha;
+    c.mode = static_cast<int32_t>(cfg.mode);            // plain = 0, sign_aware = 1
+    c.drop_mode = static_cast<int32_t>(cfg.drop_mode);  // value_range = 0, count_quantile = 1
+    c.drop_fraction = cfg.drop_fraction;
+    c.retain_k = static_cast<int64_t>(cfg.retain_k);
+    c.has_chains_override = cfg.chains_override.has_value() ? 1 : 0;
+    c.chains_override = cfg.chains_override.value_or(0);
+    c.has_max_len_override = cfg.max_len_override.has_value() ? 1 : 0;
+    c.max_len_override = cfg.max_len_override.value_or(0);
+    c.master_seed = cfg.master_seed;
+    c.rng_mode = opt.rng_mode;
+    c.device = opt.device;
+    return c;
+}
+
+template <class SplitErrorT>
+[[noreturn]] inline void rethrow(int code, const char* msg) {
+    switch (code) {
+        case MCMI_EINVAL: throw std::invalid_argument(msg);
+        case MCMI_ESPLIT: throw SplitErrorT(msg);
+        case MCMI_ERANGE: throw std::out_of_range(msg);
+        case MCMI_ENOMEM: throw std::bad_alloc();
+        default: throw std::runtime_error(std::string("mcmi: ") + msg);
+    }
+}
+
+template <class ApproxInverseT, class SplitErrorT, class CsrT, class CfgT>
+ApproxInverseT compute_preconditioner(const CsrT& b, const CfgT& cfg, const Options& opt = {}) {
+    const mcmi_config c = to_config(cfg, opt);
+    const mcmi_csr_view view{static_cast<int64_t>(b.n),
+                             reinterpret_cast<const int64_t*>(b.row_ptr.data()),
+                             reinterpret_cast<const int64_t*>(b.col_idx.data()), b.values.data()};
+    char err[512] = {0};
+    mcmi_result* res = nullptr;
+    const int code = mcmi_build(&view, &c, &res, err, sizeof err);
+    if (code != MCMI_OK) rethrow<SplitErrorT>(code, err);
+    struct Guard {
+        mcmi_result* r;
+        ~Guard() { mcmi_result_free(r); }
+    } guard{res};
+    int64_t n = 0, nnz = 0;
+    mcmi_result_sizes(res, &n, &nnz);
+    ApproxInverseT out;
+    out.m.n = n;
+    out.m.row_ptr.resize(static_cast<size_t>(n) + 1);
+    out.m.col_idx.resize(static_cast<size_t>(nnz));
+    out.m.values.resize(static_cast<size_t>(nnz));
+    std::vector<int64_t> chains(static_cast<size_t>(n)), before(static_cast<size_t>(n));
+    int64_t n_chains = 0, max_len = 0;
+    if (mcmi_result_copy(res, reinterpret_cast<int64_t*>(out.m.row_ptr.data()),
+                         reinterpret_cast<int64_t*>(out.m.col_idx.data()), out.m.values.data(),
+                         chains.data(), before.data(), &n_chains, &max_len) != MCMI_OK)
+        throw std::runtime_error("mcmi: result copy failed");
+    out.row_meta.resize(static_cast<size_t>(n));
+    for (int64_t i = 0; i < n; ++i) {
+        out.row_meta[i].chains_used = chains[i];
+        out.row_meta[i].entries_before_retention = before[i];
+    }
+    out.config_echo = cfg;
+    out.budget_echo.n_chains = n_chains;
+    out.budget_echo.max_len = max_len;
+    out.seed_echo = cfg.master_seed;
+    return out;
+}
+
+}  // namespace compat
+}  // namespace mcmi
+
+#endif
