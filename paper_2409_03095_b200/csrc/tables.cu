@@ -36,8 +36,70 @@ constexpr int TB = 256;
 inline int grid_for(int64_t items, int per_block = TB) {
     int64_t g = (items + per_block - 1) / per_block;
     if (g < 1) g = 1;
-    if (g > 148 * 64) g = 148 * 64;  // grid-stride beyond ~64 blocks per SM
+    if (g > 148 * 8) g = 148 * 8;  // grid-stride beyond 8 blocks per SM
     return static_cast<int>(g);
+}
+
+// Block-wide reductions so each block issues ONE atomic per scalar (a per-thread
+// atomic on one address serialises ~2.4M updates at L2).
+__device__ __forceinline__ double block_max(double v) {
+    __shared__ double red[TB / 32];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL_MASK, v, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < TB / 32 ? red[threadIdx.x] : 0.0;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL_MASK, v, o));
+    }
+    __syncthreads();
+    return v;  // valid in thread 0
+}
+
+__device__ __forceinline__ double block_min(double v) {
+    __shared__ double red[TB / 32];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL_MASK, v, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < TB / 32 ? red[threadIdx.x] : __longlong_as_double(0x7ff0000000000000ll);
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v = fmin(v, __shfl_xor_sync(FULL_MASK, v, o));
+    }
+    __syncthreads();
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long block_sum_u64(unsigned long long v) {
+    __shared__ unsigned long long red[TB / 32];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < TB / 32 ? red[threadIdx.x] : 0ull;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL_MASK, v, o);
+    }
+    __syncthreads();
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long block_max_u64(unsigned long long v) {
+    __shared__ unsigned long long red[TB / 32];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL_MASK, v, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+        v = threadIdx.x < TB / 32 ? red[threadIdx.x] : 0ull;
+#pragma unroll
+        for (int o = 16; o; o >>= 1) v = max(v, __shfl_xor_sync(FULL_MASK, v, o));
+    }
+    __syncthreads();
+    return v;
 }
 
 __device__ __forceinline__ double drop_threshold(const Reductions* red, double p) {
@@ -91,7 +153,10 @@ __global__ void k_offdiag_range(TableBuildArgs a) {
             seen = true;
         }
     }
-    if (seen) {
+    (void)seen;  // an unseen thread contributes (+inf, 0), the identities
+    mn = block_min(mn);
+    mx = block_max(mx);
+    if (threadIdx.x == 0 && mx >= mn) {  // block saw at least one off-diagonal
         atomic_min_nonneg(&a.red->offmin_bits, mn);
         atomic_max_nonneg(&a.red->offmax_bits, mx);
     }
@@ -122,7 +187,8 @@ __global__ void k_rows_norm(TableBuildArgs a) {
         a.diag_val[i] = d;
         best = fmax(best, s);
     }
-    atomic_max_nonneg(&a.red->bnorm_bits, best);
+    best = block_max(best);
+    if (threadIdx.x == 0) atomic_max_nonneg(&a.red->bnorm_bits, best);
 }
 
 // Pass C: B1 = diag(B_hat), A's row counts, ||A||inf, max degree.
@@ -156,9 +222,14 @@ __global__ void k_rows_split(TableBuildArgs a) {
         max_deg = max(max_deg, cnt);
         nnz_a += cnt;
     }
-    atomic_max_nonneg(&a.red->anorm_bits, best);
-    atomicMax(&a.red->max_deg, static_cast<unsigned long long>(max_deg));
-    atomicAdd(&a.red->a_nnz, nnz_a);
+    best = block_max(best);
+    const unsigned long long md = block_max_u64(max_deg);
+    nnz_a = block_sum_u64(nnz_a);
+    if (threadIdx.x == 0) {
+        atomic_max_nonneg(&a.red->anorm_bits, best);
+        atomicMax(&a.red->max_deg, md);
+        atomicAdd(&a.red->a_nnz, nnz_a);
+    }
 }
 
 // Pass D: transition records (split.cpp:75-92 values, split.cpp:102-119
@@ -240,7 +311,8 @@ __global__ void k_cq_count(TableBuildArgs a, CqState* st) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
          i += (int64_t)gridDim.x * blockDim.x)
         for (int64_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) cnt += (a.col_idx[k] != i);
-    atomicAdd(&st->n_off, cnt);
+    cnt = block_sum_u64(cnt);
+    if (threadIdx.x == 0) atomicAdd(&st->n_off, cnt);
 }
 
 __global__ void k_cq_init(CqState* st, double p) {

@@ -33,16 +33,23 @@
 // shared memory, capacity `cap`; a row that touches more than cap_limit
 // columns is abandoned and re-run by the host on a larger tier.
 //
+// The fold of the other columns is a shuffle chain: lane of group rank i adds
+// its weight to its predecessor's running sum in round i.
+//
 // Finalize (per row, in shared memory): compact the hash, bitonic-sort by
 // column, multiply by 1/chains_run, rank for retain_top_k (diag first, |v|
 // desc, col asc), divide by b1_diag[col], prune exact zeros off the diagonal,
 // write the row to its staging slot.
 #include <climits>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.cuh"
 
 namespace mcmi {
+
+constexpr int kDefaultMinBlocks = 5;
+
 namespace {
 
 __host__ __device__ inline int round32(int x) { return (x + 31) & ~31; }
@@ -68,6 +75,7 @@ __device__ __forceinline__ int hash_slot(int* keys, unsigned mask, int shift, in
                                          int& n_new) {
     unsigned h = (static_cast<unsigned>(col) * 0x9E3779B1u) >> shift;
     volatile int* vk = keys;
+    if (vk[h] == col) return static_cast<int>(h);  // common case: already present, no collision
     for (unsigned probe = 0; probe <= mask; ++probe) {
         const int k = vk[h];
         if (k == col) return static_cast<int>(h);
@@ -119,8 +127,8 @@ __device__ __forceinline__ bool topk_before(int cj, double vj, int ci, double vi
     return cj < ci;
 }
 
-template <int MODE>
-__global__ void __launch_bounds__(256) k_walk(const WalkArgs a) {
+template <int MODE, int MINB>
+__global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = static_cast<int>(threadIdx.x & 31);
     const int warp = static_cast<int>(threadIdx.x >> 5);
@@ -361,7 +369,8 @@ __global__ void __launch_bounds__(256) k_walk(const WalkArgs a) {
                 acc_r = add_ones(acc_r, __popc(valid & ~done_mask));
             }
             // (ii) every other column: 32-position chunks of the chain-major log;
-            // equal columns grouped by __match_any_sync, leader adds in lane order.
+            // equal columns grouped by __match_any_sync; the group's left fold runs
+            // as a shuffle chain in lane (= chain-major) order.
             int n_new = 0;
             bool fail = false;
             const int span = B * S;
@@ -373,21 +382,29 @@ __global__ void __launch_bounds__(256) k_walk(const WalkArgs a) {
                 ok = ok && c >= 0 && c != rowc;  // column r was folded in (i)
                 if (!ok) c = -1 - lane;          // unique non-column tag
                 const unsigned peers = __match_any_sync(FULL_MASK, c);
-                if (ok && (__ffs(peers) - 1) == lane) {
-                    const int slot = hash_slot(sm.keys, cap_mask, shift, c, n_new);
-                    if (slot < 0) {
-                        fail = true;
-                    } else {
-                        double v = sm.vals[slot];
-                        unsigned rest = peers;
-                        while (rest) {
-                            const int b = __ffs(rest) - 1;
-                            rest &= rest - 1;
-                            v += sm.log_w[base + b];
-                        }
-                        sm.vals[slot] = v;
-                    }
+                // group rank = position of this entry among equal columns of the
+                // chunk (lane order == chain-major order); predecessor = the
+                // previous entry of the group
+                const unsigned below = peers & lt_mask;
+                const int rank = __popc(below);
+                const int pred = below ? 31 - __clz(below) : lane;
+                const int gsize = ok ? __popc(peers) : 0;
+                const int leader = __ffs(peers) - 1;
+                int slot = 0;
+                if (ok && rank == 0) {
+                    slot = hash_slot(sm.keys, cap_mask, shift, c, n_new);
+                    if (slot < 0) fail = true;
                 }
+                slot = __shfl_sync(FULL_MASK, slot, leader);
+                const double w = ok ? sm.log_w[p] : 0.0;
+                double v = w;
+                if (ok && rank == 0 && slot >= 0) v = sm.vals[slot] + w;
+                const int maxsize = __reduce_max_sync(FULL_MASK, static_cast<unsigned>(gsize));
+                for (int it = 1; it < maxsize; ++it) {  // left fold along each group, one link per round
+                    const double prev = __shfl_sync(FULL_MASK, v, pred);
+                    if (rank == it) v = prev + w;
+                }
+                if (ok && slot >= 0 && rank == gsize - 1) sm.vals[slot] = v;
                 __syncwarp();
             }
             distinct += warp_sum_int(n_new);
@@ -516,33 +533,46 @@ size_t walk_smem_bytes_per_warp(int cap, int lanes, int log_stride) {
     return static_cast<size_t>(cap + round32(lanes * log_stride)) * 12;
 }
 
-cudaError_t launch_walk(const WalkArgs& a, int warps_per_block, int num_sms, cudaStream_t s) {
-    if (a.n_work <= 0) return cudaSuccess;
+template <int MODE, int MINB>
+cudaError_t launch_walk_t(const WalkArgs& a, int warps_per_block, int num_sms, cudaStream_t s) {
     const size_t smem = walk_smem_bytes_per_warp(a.cap, a.lanes, a.log_stride) * warps_per_block;
     const int threads = warps_per_block * 32;
+    cudaError_t e = cudaFuncSetAttribute(k_walk<MODE, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem));
+    if (e != cudaSuccess) return e;
     int per_sm = 0;
-    cudaError_t e;
-    if (a.rng_mode == 0) {
-        e = cudaFuncSetAttribute(k_walk<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<0>, threads, smem);
-    } else {
-        e = cudaFuncSetAttribute(k_walk<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem));
-        if (e != cudaSuccess) return e;
-        e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<1>, threads, smem);
-    }
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<MODE, MINB>, threads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     int64_t blocks = static_cast<int64_t>(per_sm) * num_sms;
     const int64_t need = (a.n_work + warps_per_block - 1) / warps_per_block;
     if (blocks > need) blocks = need;
-    if (a.rng_mode == 0)
-        k_walk<0><<<static_cast<unsigned>(blocks), threads, smem, s>>>(a);
-    else
-        k_walk<1><<<static_cast<unsigned>(blocks), threads, smem, s>>>(a);
+    k_walk<MODE, MINB><<<static_cast<unsigned>(blocks), threads, smem, s>>>(a);
     return cudaGetLastError();
+}
+
+// MCMI_WALK_MINB (env, tuning only) selects the __launch_bounds__ min-blocks
+// variant: 4 = 64 regs (32 warps/SM), 5 = 48 regs (40 warps), 6 = 40 regs (48 warps).
+int walk_minb() {
+    static int v = [] {
+        const char* e = getenv("MCMI_WALK_MINB");
+        const int x = e ? atoi(e) : kDefaultMinBlocks;
+        return (x == 4 || x == 5 || x == 6) ? x : kDefaultMinBlocks;
+    }();
+    return v;
+}
+
+cudaError_t launch_walk(const WalkArgs& a, int warps_per_block, int num_sms, cudaStream_t s) {
+    if (a.n_work <= 0) return cudaSuccess;
+    const int mb = walk_minb();
+    if (a.rng_mode == 0) {
+        if (mb == 5) return launch_walk_t<0, 5>(a, warps_per_block, num_sms, s);
+        if (mb == 6) return launch_walk_t<0, 6>(a, warps_per_block, num_sms, s);
+        return launch_walk_t<0, 4>(a, warps_per_block, num_sms, s);
+    }
+    if (mb == 5) return launch_walk_t<1, 5>(a, warps_per_block, num_sms, s);
+    if (mb == 6) return launch_walk_t<1, 6>(a, warps_per_block, num_sms, s);
+    return launch_walk_t<1, 4>(a, warps_per_block, num_sms, s);
 }
 
 }  // namespace mcmi
