@@ -92,18 +92,53 @@ __device__ __forceinline__ int hash_slot(int* keys, unsigned mask, int shift, in
     return -1;
 }
 
-// acc += 1.0, k times, with the rounding of k sequential additions.  When
-// acc >= 1 and acc + k stays in acc's binade, every intermediate sum is a
-// representable integer multiple of ulp(acc), so one addition is exact; a
-// binade crossing (~log2(N) times per row) takes the sequential path.
+// acc += 1.0, k times, with the rounding of k sequential additions.  For
+// 1 <= acc < 2^53, every sum that stays below the next power of two 2^(e+1) is
+// an exactly representable multiple of ulp(acc), so those additions collapse
+// into one exact addition; the addition that crosses 2^(e+1) is performed on
+// its own (it may round).  A run therefore costs O(binade crossings), not O(k).
 __device__ __forceinline__ double add_ones(double acc, int k) {
-    if (k <= 0) return acc;
-    if (acc >= 1.0 && acc < 0x1.0p53) {
+    if (acc >= 1.0 && acc < 0x1.0p53) {  // common case: no binade crossing
         const double t = acc + static_cast<double>(k);
         if ((__double_as_longlong(t) >> 52) == (__double_as_longlong(acc) >> 52)) return t;
     }
-    for (; k > 0; --k) acc += 1.0;
+    while (k > 0) {
+        if (!(acc >= 1.0 && acc < 0x1.0p53)) {  // acc == 0 (row start) or out of range
+            acc += 1.0;
+            --k;
+            continue;
+        }
+        const double top = __longlong_as_double((__double_as_longlong(acc) & 0x7ff0000000000000ll) +
+                                                0x0010000000000000ll);  // 2^(e+1)
+        const double room = top - acc;  // exact: acc and top share the ulp grid of acc
+        // additions that keep the sum below top: i < room
+        const double fit = ceil(room) - 1.0;
+        const int j = fit < static_cast<double>(k) ? static_cast<int>(fit) : k;
+        if (j > 0) {
+            acc += static_cast<double>(j);  // exact
+            k -= j;
+        }
+        if (k > 0) {  // the crossing addition, rounded like the reference's
+            acc += 1.0;
+            --k;
+        }
+    }
     return acc;
+}
+
+// Keeps the lowest `keep` set bits of mask (keep >= 0).
+__device__ __forceinline__ unsigned lowest_bits(unsigned mask, int keep) {
+    if (__popc(mask) <= keep) return mask;
+    if (keep <= 0) return 0u;
+    // position of the keep-th set bit by binary search on prefix popcounts
+    int lo = 0, hi = 32;  // answer in [lo, hi): smallest p with popc(mask & ((2<<p)-1)) >= keep
+    while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        const unsigned pre = mid >= 32 ? mask : (mask & ((1u << mid) - 1u));
+        if (__popc(pre) >= keep) hi = mid;
+        else lo = mid;
+    }
+    return hi >= 32 ? mask : (mask & ((1u << hi) - 1u));
 }
 
 __device__ __forceinline__ int warp_sum_int(int v) {
@@ -198,6 +233,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             int m = 0;              // step deposits logged (W0 = 1 at (r, r) is implicit)
             unsigned retm = 0;      // bit t: step deposit t went back to column r (t < 32)
             bool ret_hi = false;    // a return at t >= 32
+            double ret_w = 0.0;     // weight of the first return (the only one when L <= 2)
             int state = rowc;
             double w = 1.0;
             unsigned draws = 0;
@@ -287,6 +323,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 lw[m] = w;
                 ++m;
                 if (state == rowc) {
+                    if (retm == 0 && !ret_hi) ret_w = w;
                     if (m <= 32) retm |= 1u << (m - 1);
                     else ret_hi = true;
                 }
@@ -327,8 +364,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 valid = __ballot_sync(FULL_MASK, active);
             }
             const int64_t remaining = N - chains_done;
-            while (static_cast<int64_t>(__popc(valid)) > remaining)
-                valid &= ~(1u << (31 - __clz(valid)));
+            if (remaining < 32) valid = lowest_bits(valid, static_cast<int>(remaining));
             const bool mine = (valid >> lane) & 1u;
             if (mine) {
                 row_steps += lane_steps;
@@ -346,27 +382,46 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             // (i) column r: W0 = +1.0 per valid chain plus its returns, in
             // chain order, folded in a register (warp-uniform).
             {
-                unsigned rl = __ballot_sync(FULL_MASK, mine && (retm != 0 || ret_hi));
-                unsigned done_mask = 0;  // lanes already folded
-                while (rl) {
-                    const int j = __ffs(rl) - 1;
-                    rl &= rl - 1;
-                    acc_r = add_ones(acc_r, __popc(valid & ((1u << j) - 1u) & ~done_mask) + 1);
-                    unsigned rm = __shfl_sync(FULL_MASK, retm, j);
-                    const bool hi = __shfl_sync(FULL_MASK, static_cast<int>(ret_hi), j) != 0;
-                    while (rm) {
-                        const int t1 = __ffs(rm) - 1;
-                        rm &= rm - 1;
-                        acc_r += sm.log_w[j * S + t1];
+                const unsigned rl = __ballot_sync(FULL_MASK, mine && (retm != 0 || ret_hi));
+                if (rl == 0) {
+                    acc_r = add_ones(acc_r, __popc(valid));
+                } else {
+                    const unsigned multi = __ballot_sync(FULL_MASK, mine && ((retm & (retm - 1)) != 0 || ret_hi));
+                    // W0 additions owed before this lane's return: valid chains after
+                    // the previous returning lane, up to and including this one
+                    const unsigned prevs = rl & lt_mask;
+                    const unsigned prev_mask = prevs ? ((2u << (31 - __clz(prevs))) - 1u) : 0u;
+                    const int run = __popc(valid & lt_mask & ~prev_mask) + 1;
+                    unsigned todo = rl;
+                    while (todo) {
+                        const int j = __ffs(todo) - 1;
+                        todo &= todo - 1;
+                        acc_r = add_ones(acc_r, __shfl_sync(FULL_MASK, run, j));
+                        acc_r += __shfl_sync(FULL_MASK, ret_w, j);  // first return of chain j
+                        if ((multi >> j) & 1u) {  // later returns of chain j, in step order
+                            const unsigned rm = __shfl_sync(FULL_MASK, retm, j);
+                            const bool hi = __shfl_sync(FULL_MASK, static_cast<int>(ret_hi), j) != 0;
+                            unsigned rest = rm & (rm - 1);
+                            while (rest) {
+                                const int t1 = __ffs(rest) - 1;
+                                rest &= rest - 1;
+                                acc_r += sm.log_w[j * S + t1];
+                            }
+                            if (hi) {  // returns at steps >= 32 (max_len > 32 only)
+                                bool skip = rm == 0;  // the first return was at a step >= 32
+                                const int mj = __shfl_sync(FULL_MASK, m, j);
+                                for (int t1 = 32; t1 < mj; ++t1)
+                                    if (sm.log_col[j * S + t1] == rowc) {
+                                        if (skip) skip = false;
+                                        else acc_r += sm.log_w[j * S + t1];
+                                    }
+                            }
+                        }
                     }
-                    if (hi) {
-                        const int mj = __shfl_sync(FULL_MASK, m, j);
-                        for (int t1 = 32; t1 < mj; ++t1)
-                            if (sm.log_col[j * S + t1] == rowc) acc_r += sm.log_w[j * S + t1];
-                    }
-                    done_mask = (j == 31) ? FULL_MASK : ((1u << (j + 1)) - 1u);
+                    const int last = 31 - __clz(rl);
+                    const unsigned upto = last == 31 ? FULL_MASK : ((2u << last) - 1u);
+                    acc_r = add_ones(acc_r, __popc(valid & ~upto));
                 }
-                acc_r = add_ones(acc_r, __popc(valid & ~done_mask));
             }
             // (ii) every other column: 32-position chunks of the chain-major log;
             // equal columns grouped by __match_any_sync; the group's left fold runs
@@ -448,31 +503,46 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             __syncwarp();
         }
         const int s = distinct;
-        int P = 32;
-        while (P < s) P <<= 1;
-        for (int i = s + lane; i < P; i += 32) {
-            sm.keys[i] = INT_MAX;
-            sm.vals[i] = 0.0;
-        }
-        __syncwarp();
-        // bitonic sort by column
-        for (int kb = 2; kb <= P; kb <<= 1) {
-            for (int jb = kb >> 1; jb > 0; jb >>= 1) {
-                for (int i = lane; i < P; i += 32) {
-                    const int ixj = i ^ jb;
-                    if (ixj > i) {
-                        const int ka = sm.keys[i], kc = sm.keys[ixj];
-                        const bool up = (i & kb) == 0;
-                        if ((ka > kc) == up) {
-                            const double va = sm.vals[i];
-                            sm.keys[i] = kc;
-                            sm.keys[ixj] = ka;
-                            sm.vals[i] = sm.vals[ixj];
-                            sm.vals[ixj] = va;
+        if (s <= 32) {
+            // rank sort in registers: columns are distinct, so each entry's
+            // position is the number of smaller columns
+            const int kk = lane < s ? sm.keys[lane] : INT_MAX;
+            const double vv = lane < s ? sm.vals[lane] : 0.0;
+            int pos = 0;
+            for (int j = 0; j < s; ++j) pos += __shfl_sync(FULL_MASK, kk, j) < kk;
+            __syncwarp();
+            if (lane < s) {
+                sm.keys[pos] = kk;
+                sm.vals[pos] = vv;
+            }
+            __syncwarp();
+        } else {
+            int P = 64;
+            while (P < s) P <<= 1;
+            for (int i = s + lane; i < P; i += 32) {
+                sm.keys[i] = INT_MAX;
+                sm.vals[i] = 0.0;
+            }
+            __syncwarp();
+            // bitonic sort by column
+            for (int kb = 2; kb <= P; kb <<= 1) {
+                for (int jb = kb >> 1; jb > 0; jb >>= 1) {
+                    for (int i = lane; i < P; i += 32) {
+                        const int ixj = i ^ jb;
+                        if (ixj > i) {
+                            const int ka = sm.keys[i], kc = sm.keys[ixj];
+                            const bool up = (i & kb) == 0;
+                            if ((ka > kc) == up) {
+                                const double va = sm.vals[i];
+                                sm.keys[i] = kc;
+                                sm.keys[ixj] = ka;
+                                sm.vals[i] = sm.vals[ixj];
+                                sm.vals[ixj] = va;
+                            }
                         }
                     }
+                    __syncwarp();
                 }
-                __syncwarp();
             }
         }
         const double inv_n = 1.0 / static_cast<double>(chains_run);  // mc_engine.cpp:109

@@ -27,8 +27,11 @@ def main():
         if not header or len(r) < 8 or not r[0].isdigit():
             continue
         d = dict(zip(header[4:], r[4:]))
-        s = int(d.get("Warp Stall Sampling (All Samples)", "0") or 0)
-        ins = int(d.get("Instructions Executed", "0") or 0)
+        try:
+            s = int(d.get("Warp Stall Sampling (All Samples)", "0") or 0)
+            ins = int(d.get("Instructions Executed", "0") or 0)
+        except ValueError:
+            continue
         stalls = {k[6:]: int(v) for k, v in d.items() if k.startswith("stall_") and "Not Issued" not in k
                   and v.isdigit() and int(v) > 0}
         top3 = sorted(stalls.items(), key=lambda kv: -kv[1])[:3]
