@@ -88,6 +88,9 @@ def lib():
         L.ref_rng_u32.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, C.POINTER(C.c_uint32)]
         L.ref_rng_double.argtypes = [C.c_uint64, C.c_uint64, C.c_int64, _f64p]
         L.ref_max_threads.restype = C.c_int
+        L.ref_solve.argtypes = [C.c_int64, _i64p, _i64p, _f64p, C.c_int64, _i64p, _i64p, _f64p, C.c_int,
+                                C.c_double, C.c_int64, C.c_int64, _i64p, C.POINTER(C.c_int), _f64p,
+                                C.c_char_p, C.c_size_t]
         _lib = L
     return _lib
 
@@ -329,3 +332,23 @@ def rng_double(seed: int, sid: int, count: int) -> np.ndarray:
 
 def max_threads() -> int:
     return lib().ref_max_threads()
+
+
+def solve(b: Csr, m: Csr | None, method: str = "gmres", rel_tol: float = 1e-6, max_iters: int = 30000,
+          restart: int = 50):
+    """mcspai::solve (solvers.cpp:240-244) with rhs = B*1 (ones_product_rhs):
+    returns (iterations, converged, final_rel_residual)."""
+    L = lib()
+    rp, ci, v = b.args()
+    if m is not None:
+        mrp, mci, mv = m.args()
+        nm = m.n
+    else:
+        mrp, mci, mv = np.zeros(1, np.int64), np.zeros(1, np.int64), np.zeros(1)
+        nm = -1
+    it, conv, res = C.c_int64(), C.c_int(), C.c_double()
+    err = C.create_string_buffer(512)
+    _check(L.ref_solve(b.n, _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p), nm, _p(mrp, _i64p), _p(mci, _i64p),
+                       _p(mv, _f64p), 0 if method == "gmres" else 1, rel_tol, max_iters, restart,
+                       C.byref(it), C.byref(conv), C.byref(res), err, 512), err)
+    return it.value, bool(conv.value), res.value

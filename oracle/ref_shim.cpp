@@ -18,6 +18,7 @@
 //   ref_gen            -> mcspai::make_* generators                 (synthetic.hpp:11-31)
 //   ref_write_mm       -> mcspai::write_matrix_market_file          (matrix_market.hpp:24-25)
 //   ref_read_mm        -> mcspai::read_matrix_market_file           (matrix_market.hpp:19-20)
+//   ref_solve          -> mcspai::solve (gmres / bicgstab), rhs = B*1  (solvers.hpp:35-46)
 // Exceptions are mapped to status codes: 1 invalid_argument, 2 SplitError,
 // 3 out_of_range, 4 other.
 #include <cstdint>
@@ -30,6 +31,7 @@
 #include "mcspai/csr.hpp"
 #include "mcspai/matrix_market.hpp"
 #include "mcspai/mc_engine.hpp"
+#include "mcspai/solvers.hpp"
 #include "mcspai/split.hpp"
 #include "mcspai/synthetic.hpp"
 
@@ -289,6 +291,30 @@ int64_t ref_retain_top_k(int64_t len, int64_t* cols, double* vals, int64_t k,
         vals[i] = kept[i].second;
     }
     return static_cast<int64_t>(kept.size());
+}
+
+// ---- validation solvers (the consumer of M; iteration-count parity tier) ----
+// method 0 gmres, 1 bicgstab; precond may be null (n_m < 0).  rhs = B * ones.
+int ref_solve(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, int64_t n_m,
+              const int64_t* mrp, const int64_t* mci, const double* mv, int method,
+              double rel_tol, int64_t max_iters, int64_t restart, int64_t* iterations,
+              int* converged, double* final_rel_residual, char* err, size_t errlen) {
+    return guarded(
+        [&] {
+            const CsrMatrix b = to_csr(n, rp, ci, v);
+            CsrMatrix m;
+            if (n_m >= 0) m = to_csr(n_m, mrp, mci, mv);
+            SolverConfig cfg;
+            cfg.method = method == 0 ? SolverMethod::gmres : SolverMethod::bicgstab;
+            cfg.rel_tol = rel_tol;
+            cfg.max_iters = max_iters;
+            cfg.restart = restart;
+            const SolveReport r = solve(b, ones_product_rhs(b), n_m >= 0 ? &m : nullptr, cfg);
+            *iterations = r.iterations;
+            *converged = r.converged ? 1 : 0;
+            *final_rel_residual = r.final_rel_residual;
+        },
+        err, errlen);
 }
 
 // ---- RNG ----------------------------------------------------------------------

@@ -153,6 +153,7 @@ struct mcmi_engine {
     DevBuf red, diag_val, a_cnt, a_off, keep, rec, ent, colA, b1, scan_tmp, cq_tmp;
     DevBuf stage_col, stage_val, row_cnt, row_src, chains_used, entries_before, counters;
     DevBuf ovf[2];
+    DevBuf gscratch;  // global accumulator tier
     DevBuf out_rp, out_col, out_val;
     Reductions* h_red = nullptr;          // pinned
     unsigned long long* h_ctr = nullptr;  // pinned [8]
@@ -188,7 +189,7 @@ void engine_release(mcmi_engine* e) {
     for (DevBuf* b : {&e->red, &e->diag_val, &e->a_cnt, &e->a_off, &e->keep, &e->rec, &e->ent,
                       &e->colA, &e->b1, &e->scan_tmp, &e->cq_tmp, &e->stage_col, &e->stage_val,
                       &e->row_cnt, &e->row_src, &e->chains_used, &e->entries_before,
-                      &e->counters, &e->ovf[0], &e->ovf[1], &e->out_rp, &e->out_col,
+                      &e->counters, &e->ovf[0], &e->ovf[1], &e->gscratch, &e->out_rp, &e->out_col,
                       &e->out_val})
         b->release();
     for (auto& ev : e->ev)
@@ -203,6 +204,7 @@ constexpr int kLogMax = 256;  // deposit-log entries per warp (shared memory)
 
 struct Tier {
     int cap, cap_limit, lanes, log_stride, warps_per_block;
+    bool global = false;  // accumulator + log in global scratch
 };
 
 Tier make_tier(int cap, int64_t max_len) {
@@ -215,6 +217,20 @@ Tier make_tier(int cap, int64_t max_len) {
     t.lanes = std::max(1, std::min(32, logmax / t.log_stride));
     const size_t per_warp = walk_smem_bytes_per_warp(t.cap, t.lanes, t.log_stride);
     t.warps_per_block = static_cast<int>(std::max<size_t>(1, std::min<size_t>(8, (96u * 1024u) / per_warp)));
+    return t;
+}
+
+// Global-memory tier: any row size, full-width batches for long walks.
+Tier make_global_tier(int64_t bound, int64_t max_len) {
+    Tier t;
+    int64_t cap = 8192;
+    while (cap - cap / 4 < bound && cap < (int64_t{1} << 30)) cap <<= 1;
+    t.cap = static_cast<int>(cap);
+    t.cap_limit = t.cap - t.cap / 4;
+    t.log_stride = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, max_len), INT_MAX / 64));
+    t.lanes = 32;
+    t.warps_per_block = 8;
+    t.global = true;
     return t;
 }
 
@@ -342,6 +358,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     tiers.push_back(make_tier(first_cap, L));
     for (int c : kTierCaps)
         if (c > first_cap && (tiers.back().cap_limit < bound)) tiers.push_back(make_tier(c, L));
+    if (tiers.back().cap_limit < bound) tiers.push_back(make_global_tier(bound, L));
     st.hash_cap = first_cap;
 
     MCMI_TRY(e->row_cnt.ensure(std::max<int64_t>(rows, 1) * sizeof(int)), "alloc row_cnt");
@@ -387,6 +404,20 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         wa.log_stride = t.log_stride;
         wa.log_magic = static_cast<unsigned>((0x100000000ull + t.log_stride - 1) / t.log_stride);
         wa.ell0 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(L, 2)));
+        wa.gscratch = nullptr;
+        int64_t max_warps = 0;
+        if (t.global) {
+            size_t free_b = 0, total_b = 0;
+            MCMI_TRY(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+            const size_t per_warp = walk_global_bytes_per_warp(t.cap, t.log_stride);
+            const size_t budget = std::min<size_t>(size_t{16} << 30, free_b / 2);
+            max_warps = std::min<int64_t>(static_cast<int64_t>(budget / per_warp),
+                                          static_cast<int64_t>(e->num_sms) * 32);
+            if (max_warps < 1) return fail(MCMI_ENOMEM, "accumulator row too large for device memory");
+            max_warps = std::max<int64_t>(8, max_warps / 8 * 8);
+            MCMI_TRY(e->gscratch.ensure(static_cast<size_t>(max_warps) * per_warp), "alloc accumulator scratch");
+            wa.gscratch = e->gscratch.as<unsigned char>();
+        }
         wa.stage_col = e->stage_col.as<int>();
         wa.stage_val = e->stage_val.as<double>();
         wa.stage_base = pool_used;
@@ -398,7 +429,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         wa.counters = e->counters.as<unsigned long long>();
         wa.overflow_list = e->ovf[cur].as<int>();
         MCMI_TRY(cudaEventRecord(e->ev[4], s), "cudaEventRecord");
-        MCMI_TRY(launch_walk(wa, t.warps_per_block, e->num_sms, s), "walk kernel");
+        MCMI_TRY(launch_walk(wa, t.warps_per_block, e->num_sms, t.global, max_warps, s), "walk kernel");
         MCMI_TRY(cudaEventRecord(e->ev[5], s), "cudaEventRecord");
         st.launches += 1;
         MCMI_TRY(cudaMemcpyAsync(e->h_ctr, e->counters.p, 8 * sizeof(unsigned long long),
@@ -418,9 +449,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         cur ^= 1;
     }
     if (work > 0)
-        return fail(MCMI_ENOMEM, std::to_string(work) +
-                                     " rows touch more than 3072 distinct columns; the "
-                                     "accumulator tier for such rows is not available");
+        return fail(MCMI_ENOMEM, std::to_string(work) + " rows overflowed every accumulator tier");
     st.walk_steps = static_cast<int64_t>(total_steps);
     st.walk_deg_sum = static_cast<int64_t>(total_deg);
     MCMI_TRY(cudaEventRecord(e->ev[2], s), "cudaEventRecord");

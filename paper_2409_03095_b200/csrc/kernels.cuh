@@ -79,6 +79,7 @@ struct WalkArgs {
     int log_stride;         // max(max_len, 1) step deposits per chain
     unsigned log_magic;     // ceil(2^32 / log_stride): p / log_stride == __umulhi(p, log_magic)
     int ell0;               // initial speculative draw stride (reference-stream mode)
+    unsigned char* gscratch;  // global-tier per-warp accumulator + log (nullptr for smem tiers)
     // outputs, indexed by local row (row - row_begin)
     int* stage_col;
     double* stage_val;
@@ -99,7 +100,9 @@ cudaError_t launch_count_quantile(const TableBuildArgs& a, int64_t nnz, int64_t 
                                   void* scratch, size_t scratch_bytes, cudaStream_t s);
 size_t count_quantile_scratch_bytes(int64_t nnz);
 size_t walk_smem_bytes_per_warp(int cap, int lanes, int log_stride);
-cudaError_t launch_walk(const WalkArgs& a, int warps_per_block, int num_sms, cudaStream_t s);
+size_t walk_global_bytes_per_warp(int cap, int log_stride);
+cudaError_t launch_walk(const WalkArgs& a, int warps_per_block, int num_sms, bool global_tier,
+                        int64_t max_warps, cudaStream_t s);
 
 // Exclusive scans (assemble.cu).
 size_t scan_scratch_bytes(int64_t n);

@@ -40,6 +40,7 @@
 // column, multiply by 1/chains_run, rank for retain_top_k (diag first, |v|
 // desc, col asc), divide by b1_diag[col], prune exact zeros off the diagonal,
 // write the row to its staging slot.
+#include <algorithm>
 #include <climits>
 #include <cstdlib>
 
@@ -162,7 +163,176 @@ __device__ __forceinline__ bool topk_before(int cj, double vj, int ci, double vi
     return cj < ci;
 }
 
-template <int MODE, int MINB>
+__device__ __forceinline__ unsigned long long topk_key(int c, double v, int diag) {
+    return c == diag ? ~0ull : static_cast<unsigned long long>(__double_as_longlong(fabs(v)));
+}
+
+// Warp-cooperative selection of the first k entries of [0, s) in retain_top_k
+// order (mc_engine.cpp:131-139: diagonal first, |v| desc, column asc) by a
+// radix select over the 64-bit key (8 passes) and, for ties at the threshold,
+// over the column (4 passes).  Entry i is kept iff key > T || (key == T &&
+// col <= Tc).  hist: 256 scratch words.  O(s) instead of the O(s^2) ranking.
+__device__ void radix_topk(const int* keys, const double* vals, int s, int k, int diag,
+                           unsigned* hist, unsigned long long& T, int& Tc) {
+    const int lane = static_cast<int>(threadIdx.x & 31);
+    unsigned long long prefix = 0, mask = 0;
+    unsigned need = static_cast<unsigned>(k);
+    unsigned eq = 0;  // entries matching the full prefix after the last pass
+    for (int shift = 56; shift >= 0; shift -= 8) {
+        for (int b = lane; b < 256; b += 32) hist[b] = 0;
+        __syncwarp();
+        for (int i = lane; i < s; i += 32) {
+            const unsigned long long key = topk_key(keys[i], vals[i], diag);
+            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+        }
+        __syncwarp();
+        unsigned c[8], tot = 0;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {  // lane owns digits 255-8l .. 248-8l (descending)
+            c[j] = hist[255 - 8 * lane - j];
+            tot += c[j];
+        }
+        unsigned incl = tot;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned nb = __shfl_up_sync(FULL_MASK, incl, o);
+            if (lane >= o) incl += nb;
+        }
+        const unsigned excl = incl - tot;
+        const unsigned owner = __ballot_sync(FULL_MASK, excl < need && need <= incl);
+        const int src = __ffs(owner) - 1;
+        int d = 0;
+        unsigned above = 0, cnt = 0;
+        if (lane == src) {
+            unsigned cum = excl;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                if (cum + c[j] >= need) {
+                    d = 255 - 8 * lane - j;
+                    above = cum;
+                    cnt = c[j];
+                    break;
+                }
+                cum += c[j];
+            }
+        }
+        d = __shfl_sync(FULL_MASK, d, src);
+        above = __shfl_sync(FULL_MASK, above, src);
+        eq = __shfl_sync(FULL_MASK, cnt, src);
+        need -= above;
+        prefix |= static_cast<unsigned long long>(d) << shift;
+        mask |= 0xffull << shift;
+        __syncwarp();
+    }
+    T = prefix;
+    Tc = INT_MAX;
+    if (eq > need) {  // keep the `need` smallest columns among the ties
+        unsigned cprefix = 0, cmask = 0;
+        for (int shift = 24; shift >= 0; shift -= 8) {
+            for (int b = lane; b < 256; b += 32) hist[b] = 0;
+            __syncwarp();
+            for (int i = lane; i < s; i += 32) {
+                const unsigned col = static_cast<unsigned>(keys[i]);
+                if (topk_key(keys[i], vals[i], diag) == T && (col & cmask) == cprefix)
+                    atomicAdd(&hist[(col >> shift) & 255u], 1u);
+            }
+            __syncwarp();
+            unsigned c[8], tot = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {  // ascending digits 8l .. 8l+7
+                c[j] = hist[8 * lane + j];
+                tot += c[j];
+            }
+            unsigned incl = tot;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned nb = __shfl_up_sync(FULL_MASK, incl, o);
+                if (lane >= o) incl += nb;
+            }
+            const unsigned excl = incl - tot;
+            const unsigned owner = __ballot_sync(FULL_MASK, excl < need && need <= incl);
+            const int src = __ffs(owner) - 1;
+            int d = 0;
+            unsigned below = 0;
+            if (lane == src) {
+                unsigned cum = excl;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    if (cum + c[j] >= need) {
+                        d = 8 * lane + j;
+                        below = cum;
+                        break;
+                    }
+                    cum += c[j];
+                }
+            }
+            d = __shfl_sync(FULL_MASK, d, src);
+            below = __shfl_sync(FULL_MASK, below, src);
+            need -= below;
+            cprefix |= static_cast<unsigned>(d) << shift;
+            cmask |= 0xffu << shift;
+            __syncwarp();
+        }
+        Tc = static_cast<int>(cprefix);
+    }
+}
+
+// Bitonic sort of (keys, vals)[0, P) by key, P a power of two >= 64.
+__device__ void warp_bitonic(int* keys, double* vals, int P) {
+    const int lane = static_cast<int>(threadIdx.x & 31);
+    for (int kb = 2; kb <= P; kb <<= 1) {
+        for (int jb = kb >> 1; jb > 0; jb >>= 1) {
+            for (int i = lane; i < P; i += 32) {
+                const int ixj = i ^ jb;
+                if (ixj > i) {
+                    const int ka = keys[i], kc = keys[ixj];
+                    const bool up = (i & kb) == 0;
+                    if ((ka > kc) == up) {
+                        const double va = vals[i];
+                        keys[i] = kc;
+                        keys[ixj] = ka;
+                        vals[i] = vals[ixj];
+                        vals[ixj] = va;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+// Sorts (keys, vals)[0, s) by column: register rank sort for s <= 32, bitonic
+// otherwise (pads [s, P) with INT_MAX); returns the padded length touched.
+__device__ int sort_by_column(int* keys, double* vals, int s) {
+    const int lane = static_cast<int>(threadIdx.x & 31);
+    if (s <= 32) {
+        // columns are distinct: an entry's position is the number of smaller columns
+        const int kk = lane < s ? keys[lane] : INT_MAX;
+        const double vv = lane < s ? vals[lane] : 0.0;
+        int pos = 0;
+        for (int j = 0; j < s; ++j) pos += __shfl_sync(FULL_MASK, kk, j) < kk;
+        __syncwarp();
+        if (lane < s) {
+            keys[pos] = kk;
+            vals[pos] = vv;
+        }
+        __syncwarp();
+        return s;
+    }
+    int P = 64;
+    while (P < s) P <<= 1;
+    for (int i = s + lane; i < P; i += 32) {
+        keys[i] = INT_MAX;
+        vals[i] = 0.0;
+    }
+    __syncwarp();
+    warp_bitonic(keys, vals, P);
+    return P;
+}
+
+constexpr int kRankTopkMax = 256;  // above this row length retain_top_k uses radix_topk
+
+template <int MODE, int MINB, bool GL>
 __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = static_cast<int>(threadIdx.x & 31);
@@ -172,7 +342,10 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     const int B = a.lanes;                      // chains per batch
     const int logn = round32(B * S);
     const size_t per_warp = static_cast<size_t>(cap + logn) * 12;
-    const WarpSmem sm = carve(smem_raw + per_warp * warp, cap, logn);
+    // GL: per-warp accumulator + log in global scratch (large rows / long walks)
+    unsigned char* wbase = GL ? a.gscratch + per_warp * (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp)
+                              : smem_raw + per_warp * warp;
+    const WarpSmem sm = carve(wbase, cap, logn);
     const unsigned cap_mask = static_cast<unsigned>(cap - 1);
     const int shift = 32 - (31 - __clz(cap));
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -186,6 +359,13 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
 
     unsigned long long tot_steps = 0, tot_deg = 0;
 
+    // the accumulator starts empty; finalize restores it to empty after each row
+    for (int i = lane; i < cap; i += 32) {
+        sm.keys[i] = EMPTY_KEY;
+        sm.vals[i] = 0.0;
+    }
+    __syncwarp();
+
     for (;;) {
         long long wi = 0;
         if (lane == 0) wi = static_cast<long long>(atomicAdd(&a.counters[0], 1ull));
@@ -194,11 +374,6 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
         const int64_t row = a.row_list ? static_cast<int64_t>(a.row_list[wi]) : a.row_begin + wi;
         const int rowc = static_cast<int>(row);
 
-        for (int i = lane; i < cap; i += 32) {
-            sm.keys[i] = EMPTY_KEY;
-            sm.vals[i] = 0.0;
-        }
-        __syncwarp();
         // the diagonal column's slot; its sum lives in a register (acc_r)
         int n_new0 = 0;
         int slot_r = 0;
@@ -477,6 +652,11 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 const unsigned long long q = atomicAdd(&a.counters[3], 1ull);
                 a.overflow_list[q] = rowc;
             }
+            for (int i = lane; i < cap; i += 32) {
+                sm.keys[i] = EMPTY_KEY;
+                sm.vals[i] = 0.0;
+            }
+            __syncwarp();
             continue;
         }
         tot_steps += row_steps;
@@ -485,7 +665,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
         __syncwarp();
 
         // ------------------------------------------------------ finalize
-        // compact occupied slots to [0, distinct) (in place, order-preserving)
+        // compact occupied slots to [0, s) in place, emptying the vacated slots
         int o = 0;
         for (int i0 = 0; i0 < cap; i0 += 32) {
             const int i = i0 + lane;
@@ -493,9 +673,14 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             const double vv = sm.vals[i];
             const bool occ = kk != EMPTY_KEY;
             const unsigned bal = __ballot_sync(FULL_MASK, occ);
+            const int dst = o + __popc(bal & lt_mask);
+            __syncwarp();
+            if (occ && dst != i) {
+                sm.keys[i] = EMPTY_KEY;
+                sm.vals[i] = 0.0;
+            }
             __syncwarp();
             if (occ) {
-                const int dst = o + __popc(bal & lt_mask);
                 sm.keys[dst] = kk;
                 sm.vals[dst] = vv;
             }
@@ -503,69 +688,66 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             __syncwarp();
         }
         const int s = distinct;
-        if (s <= 32) {
-            // rank sort in registers: columns are distinct, so each entry's
-            // position is the number of smaller columns
-            const int kk = lane < s ? sm.keys[lane] : INT_MAX;
-            const double vv = lane < s ? sm.vals[lane] : 0.0;
-            int pos = 0;
-            for (int j = 0; j < s; ++j) pos += __shfl_sync(FULL_MASK, kk, j) < kk;
-            __syncwarp();
-            if (lane < s) {
-                sm.keys[pos] = kk;
-                sm.vals[pos] = vv;
-            }
-            __syncwarp();
-        } else {
-            int P = 64;
-            while (P < s) P <<= 1;
-            for (int i = s + lane; i < P; i += 32) {
-                sm.keys[i] = INT_MAX;
-                sm.vals[i] = 0.0;
-            }
-            __syncwarp();
-            // bitonic sort by column
-            for (int kb = 2; kb <= P; kb <<= 1) {
-                for (int jb = kb >> 1; jb > 0; jb >>= 1) {
-                    for (int i = lane; i < P; i += 32) {
-                        const int ixj = i ^ jb;
-                        if (ixj > i) {
-                            const int ka = sm.keys[i], kc = sm.keys[ixj];
-                            const bool up = (i & kb) == 0;
-                            if ((ka > kc) == up) {
-                                const double va = sm.vals[i];
-                                sm.keys[i] = kc;
-                                sm.keys[ixj] = ka;
-                                sm.vals[i] = sm.vals[ixj];
-                                sm.vals[ixj] = va;
-                            }
-                        }
-                    }
-                    __syncwarp();
-                }
-            }
-        }
         const double inv_n = 1.0 / static_cast<double>(chains_run);  // mc_engine.cpp:109
         for (int i = lane; i < s; i += 32) sm.vals[i] = sm.vals[i] * inv_n;
         __syncwarp();
 
-        const bool keep_all = a.retain_k <= 0 || static_cast<int64_t>(s) <= a.retain_k;
+        const int64_t kret = a.retain_k;
+        bool keep_all = kret <= 0 || static_cast<int64_t>(s) <= kret;
+        int len = s;        // entries that go to the output stage (column-sorted)
+        int touched = s;    // slots [0, touched) to restore to empty afterwards
+        if (!keep_all && s > kRankTopkMax) {
+            // retain_top_k by radix selection, then sort only the kept entries
+            unsigned* hist = reinterpret_cast<unsigned*>(sm.vals + (cap - 128));  // free: s <= 3/4 cap
+            unsigned long long T;
+            int Tc;
+            radix_topk(sm.keys, sm.vals, s, static_cast<int>(kret), rowc, hist, T, Tc);
+            for (int b = lane; b < 256; b += 32) hist[b] = 0;  // restore the zeros of the vals array
+            __syncwarp();
+            int kept = 0;
+            for (int i0 = 0; i0 < s; i0 += 32) {  // stable forward compaction of the kept set
+                const int i = i0 + lane;
+                int kk = 0;
+                double vv = 0.0;
+                bool keep = false;
+                if (i < s) {
+                    kk = sm.keys[i];
+                    vv = sm.vals[i];
+                    const unsigned long long key = topk_key(kk, vv, rowc);
+                    keep = key > T || (key == T && kk <= Tc);
+                }
+                const unsigned bal = __ballot_sync(FULL_MASK, keep);
+                __syncwarp();
+                if (keep) {
+                    sm.keys[kept + __popc(bal & lt_mask)] = kk;
+                    sm.vals[kept + __popc(bal & lt_mask)] = vv;
+                }
+                kept += __popc(bal);
+                __syncwarp();
+            }
+            len = kept;
+            keep_all = true;
+            touched = max(touched, sort_by_column(sm.keys, sm.vals, len));
+        } else {
+            touched = max(touched, sort_by_column(sm.keys, sm.vals, s));
+        }
+
         const int64_t out_off = a.stage_base + wi * a.stage_stride;
         int* __restrict__ oc = a.stage_col + out_off;
         double* __restrict__ ov = a.stage_val + out_off;
         int n_out = 0;
-        for (int i0 = 0; i0 < s; i0 += 32) {
+        for (int i0 = 0; i0 < len; i0 += 32) {
             const int i = i0 + lane;
-            bool keep = i < s;
+            bool keep = i < len;
             int c = 0;
             double v = 0.0;
             if (keep) {
                 c = sm.keys[i];
                 v = sm.vals[i];
-                if (!keep_all) {
+                if (!keep_all) {  // small rows: rank in retain_top_k order
                     int64_t rank = 0;
-                    for (int j = 0; j < s; ++j) rank += topk_before(sm.keys[j], sm.vals[j], c, v, rowc);
-                    keep = rank < a.retain_k;
+                    for (int j = 0; j < len; ++j) rank += topk_before(sm.keys[j], sm.vals[j], c, v, rowc);
+                    keep = rank < kret;
                 }
             }
             if (keep) {
@@ -587,6 +769,11 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             a.entries_before[lrow] = s;
         }
         __syncwarp();
+        for (int i = lane; i < touched; i += 32) {  // back to an empty accumulator
+            sm.keys[i] = EMPTY_KEY;
+            sm.vals[i] = 0.0;
+        }
+        __syncwarp();
     }
 
     tot_steps = warp_sum_u64(tot_steps);
@@ -603,21 +790,28 @@ size_t walk_smem_bytes_per_warp(int cap, int lanes, int log_stride) {
     return static_cast<size_t>(cap + round32(lanes * log_stride)) * 12;
 }
 
-template <int MODE, int MINB>
-cudaError_t launch_walk_t(const WalkArgs& a, int warps_per_block, int num_sms, cudaStream_t s) {
-    const size_t smem = walk_smem_bytes_per_warp(a.cap, a.lanes, a.log_stride) * warps_per_block;
+size_t walk_global_bytes_per_warp(int cap, int log_stride) {
+    return walk_smem_bytes_per_warp(cap, 32, log_stride);
+}
+
+template <int MODE, int MINB, bool GL>
+cudaError_t launch_walk_t(const WalkArgs& a, int warps_per_block, int num_sms, int64_t max_warps,
+                          cudaStream_t s) {
+    const size_t smem = GL ? 0 : walk_smem_bytes_per_warp(a.cap, a.lanes, a.log_stride) * warps_per_block;
     const int threads = warps_per_block * 32;
-    cudaError_t e = cudaFuncSetAttribute(k_walk<MODE, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_walk<MODE, MINB, GL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<MODE, MINB>, threads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<MODE, MINB, GL>, threads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     int64_t blocks = static_cast<int64_t>(per_sm) * num_sms;
     const int64_t need = (a.n_work + warps_per_block - 1) / warps_per_block;
     if (blocks > need) blocks = need;
-    k_walk<MODE, MINB><<<static_cast<unsigned>(blocks), threads, smem, s>>>(a);
+    if (max_warps > 0 && blocks * warps_per_block > max_warps)
+        blocks = std::max<int64_t>(1, max_warps / warps_per_block);
+    k_walk<MODE, MINB, GL><<<static_cast<unsigned>(blocks), threads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -632,17 +826,22 @@ int walk_minb() {
     return v;
 }
 
-cudaError_t launch_walk(const WalkArgs& a, int warps_per_block, int num_sms, cudaStream_t s) {
+cudaError_t launch_walk(const WalkArgs& a, int warps_per_block, int num_sms, bool global_tier,
+                        int64_t max_warps, cudaStream_t s) {
     if (a.n_work <= 0) return cudaSuccess;
+    if (global_tier) {  // rare rows; occupancy is bounded by the scratch budget anyway
+        return a.rng_mode == 0 ? launch_walk_t<0, 4, true>(a, warps_per_block, num_sms, max_warps, s)
+                               : launch_walk_t<1, 4, true>(a, warps_per_block, num_sms, max_warps, s);
+    }
     const int mb = walk_minb();
     if (a.rng_mode == 0) {
-        if (mb == 5) return launch_walk_t<0, 5>(a, warps_per_block, num_sms, s);
-        if (mb == 6) return launch_walk_t<0, 6>(a, warps_per_block, num_sms, s);
-        return launch_walk_t<0, 4>(a, warps_per_block, num_sms, s);
+        if (mb == 5) return launch_walk_t<0, 5, false>(a, warps_per_block, num_sms, 0, s);
+        if (mb == 6) return launch_walk_t<0, 6, false>(a, warps_per_block, num_sms, 0, s);
+        return launch_walk_t<0, 4, false>(a, warps_per_block, num_sms, 0, s);
     }
-    if (mb == 5) return launch_walk_t<1, 5>(a, warps_per_block, num_sms, s);
-    if (mb == 6) return launch_walk_t<1, 6>(a, warps_per_block, num_sms, s);
-    return launch_walk_t<1, 4>(a, warps_per_block, num_sms, s);
+    if (mb == 5) return launch_walk_t<1, 5, false>(a, warps_per_block, num_sms, 0, s);
+    if (mb == 6) return launch_walk_t<1, 6, false>(a, warps_per_block, num_sms, 0, s);
+    return launch_walk_t<1, 4, false>(a, warps_per_block, num_sms, 0, s);
 }
 
 }  // namespace mcmi

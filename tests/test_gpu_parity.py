@@ -242,3 +242,54 @@ def test_full_size_row_windows_bit_identical(mc, oracle_mod, cfgname, rng):
     rows = np.repeat(np.arange(n), np.diff(inv.m.row_ptr))
     assert np.all(inv.m.values[inv.m.col_idx == rows] != 0.0)
     assert inv.stats["rows_retried"] >= 0
+
+
+@pytest.mark.parametrize("rng", [0, 1])
+@pytest.mark.parametrize("k", [0, 32, 500, 4500])
+def test_global_tier_and_radix_topk(mc, oracle_mod, ref_mod, rng, k):
+    # rows touching 4300-5100 distinct columns: beyond the largest shared-memory
+    # tier (3072), so they run on the global-memory accumulator tier; k > 256
+    # exercises the radix top-k selection, k = 0 the full column sort
+    rb = ref_mod.gen_broad_spectrum(8192, 24, 1e-4, 1.0, 3)
+    b = mc.CsrMatrix(rb.n, rb.row_ptr, rb.col_idx, rb.values)
+    cfg = mc.McConfig(alpha=1.2, delta=1e-300, chains_override=3000, max_len_override=6, retain_k=k,
+                      master_seed=11, rng_mode=rng)
+    inv = mc.compute_preconditioner(b, cfg, rows=(100, 164))
+    want = oracle_mod.compute_preconditioner(b.n, b.row_ptr, b.col_idx, b.values, row_begin=100, row_end=164,
+                                             **cfg.oracle_kwargs())
+    assert want.entries_before.max() > 3072
+    assert np.array_equal(inv.m.row_ptr, want.row_ptr)
+    assert np.array_equal(inv.m.col_idx, want.col_idx)
+    assert bits_equal(inv.m.values, want.values)
+    assert np.array_equal(inv.row_meta.entries_before_retention, want.entries_before)
+    assert inv.stats["rows_retried"] > 0
+
+
+@pytest.mark.parametrize("rng", [0, 1])
+def test_radix_topk_midsize_rows(mc, oracle_mod, rng):
+    # 300-1700 distinct columns per row with retain_k = 32: the shared-memory
+    # tiers with radix selection (rows > 256 entries)
+    n, rp, ci, v = golden_input("broad:1024:24:1e-4:1:7")
+    b = mc.CsrMatrix(n, rp, ci, v)
+    cfg = mc.McConfig(epsilon=.02, delta=.01, alpha=1.5, retain_k=32, master_seed=42, rng_mode=rng)
+    inv = mc.compute_preconditioner(b, cfg)
+    want = oracle_mod.compute_preconditioner(n, rp, ci, v, **cfg.oracle_kwargs())
+    assert want.entries_before.max() > 256
+    assert np.array_equal(inv.m.col_idx, want.col_idx) and bits_equal(inv.m.values, want.values)
+
+
+@pytest.mark.parametrize("rng", [0, 1])
+def test_long_walks(mc, oracle_mod, rng):
+    # max_len = 147: one chain per batch in the shared-memory log
+    b = mc.CsrMatrix(500, *golden_input_tridiag(500))
+    cfg = mc.McConfig(alpha=0.3, delta=1e-30, epsilon=0.3, rng_mode=rng)
+    inv = mc.compute_preconditioner(b, cfg)
+    want = oracle_mod.compute_preconditioner(b.n, b.row_ptr, b.col_idx, b.values, **cfg.oracle_kwargs())
+    assert inv.budget_echo.max_len == want.max_len == 147
+    assert np.array_equal(inv.m.col_idx, want.col_idx) and bits_equal(inv.m.values, want.values)
+
+
+def golden_input_tridiag(n):
+    from paper_2409_03095_b200 import generators as G
+    t = G.tridiagonal(n)
+    return t.row_ptr, t.col_idx, t.values
