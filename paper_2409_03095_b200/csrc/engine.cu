@@ -158,7 +158,19 @@ struct mcmi_engine {
     Reductions* h_red = nullptr;          // pinned
     unsigned long long* h_ctr = nullptr;  // pinned [8]
     int64_t* h_i64 = nullptr;             // pinned [4]
+    int64_t* h_pilot = nullptr;           // pinned pilot-row RowMeta
+    size_t h_pilot_n = 0;
     mcmi_device_csr last{};
+    int64_t* h_pilot_buf(size_t count) {
+        if (count > h_pilot_n) {
+            if (h_pilot) cudaFreeHost(h_pilot);
+            h_pilot = nullptr;
+            h_pilot_n = 0;
+            if (cudaMallocHost(&h_pilot, count * sizeof(int64_t)) != cudaSuccess) return nullptr;
+            h_pilot_n = count;
+        }
+        return h_pilot;
+    }
 };
 
 namespace {
@@ -198,6 +210,7 @@ void engine_release(mcmi_engine* e) {
     if (e->h_red) cudaFreeHost(e->h_red);
     if (e->h_ctr) cudaFreeHost(e->h_ctr);
     if (e->h_i64) cudaFreeHost(e->h_i64);
+    if (e->h_pilot) cudaFreeHost(e->h_pilot);
 }
 
 constexpr int kLogMax = 256;  // deposit-log entries per warp (shared memory)
@@ -352,14 +365,14 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     const int64_t deposits = sat_mul(N, std::max<int64_t>(L, 0));  // distinct <= 1 + N*L
     int64_t bound = std::min<int64_t>(n1, reach);
     if (deposits < INT64_MAX) bound = std::min<int64_t>(bound, deposits + 1);
-    static const int kTierCaps[] = {256, 1024, 4096};
+    static const int kTierCaps[] = {256, 1024};  // larger rows: the global tier (32 warps/SM)
     int first_cap = static_cast<int>(std::min<int64_t>(256, std::max<int64_t>(32, next_pow2((bound * 4 + 2) / 3))));
     std::vector<Tier> tiers;
     tiers.push_back(make_tier(first_cap, L));
     for (int c : kTierCaps)
         if (c > first_cap && (tiers.back().cap_limit < bound)) tiers.push_back(make_tier(c, L));
     if (tiers.back().cap_limit < bound) tiers.push_back(make_global_tier(bound, L));
-    st.hash_cap = first_cap;
+    st.hash_cap = first_cap;  // updated below if the pilot starts on a larger tier
 
     MCMI_TRY(e->row_cnt.ensure(std::max<int64_t>(rows, 1) * sizeof(int)), "alloc row_cnt");
     MCMI_TRY(e->row_src.ensure(std::max<int64_t>(rows, 1) * sizeof(int64_t)), "alloc row_src");
@@ -375,12 +388,12 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         return std::max<int64_t>(sst, 1);
     };
     int64_t pool_used = 0;
-    int64_t work = rows;
-    const int* row_list = nullptr;
     int cur = 0;
     unsigned long long total_steps = 0, total_deg = 0;
-    for (size_t ti = 0; ti < tiers.size() && work > 0; ++ti) {
-        const Tier& t = tiers[ti];
+    // Runs `work` rows (row_list, or rows row_begin+offset ...) on tier t; returns
+    // the number of rows that overflowed it (listed in ovf[cur] on return).
+    auto run_tier = [&](const Tier& t, int64_t work, const int* row_list, int64_t offset,
+                        int64_t* overflowed) -> Status {
         const int64_t stride = stride_of(t);
         const int64_t need = pool_used + work * stride;
         MCMI_TRY(e->stage_col.grow_preserve(need * sizeof(int), pool_used * sizeof(int), s), "alloc staging");
@@ -391,6 +404,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         wa.t = Tables{n, e->rec.as<uint4>(), e->ent.as<double2>(), e->colA.as<int>(), e->b1.as<double>()};
         wa.row_begin = row_begin;
         wa.row_list = row_list;
+        wa.work_offset = offset;
         wa.n_work = work;
         wa.n_chains = N;
         wa.max_len = L;
@@ -442,8 +456,63 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         total_steps += e->h_ctr[1];
         total_deg += e->h_ctr[2];
         pool_used += work * stride;
-        const int64_t overflowed = static_cast<int64_t>(e->h_ctr[3]);
-        if (ti > 0) st.rows_retried += work;
+        *overflowed = static_cast<int64_t>(e->h_ctr[3]);
+        return ok();
+    };
+
+    // Pilot: when rows may overflow the first tier, build the first rows on the
+    // last tier (which cannot overflow: its cap_limit >= bound), and start the
+    // rest on the smallest tier that held every pilot row.  Rows the pilot
+    // under-estimates still overflow into the next tiers, so results never
+    // depend on this choice.
+    size_t t0 = 0;
+    int64_t offset = 0;
+    int64_t work = rows;
+    const int64_t pilot = std::min<int64_t>(1024, rows / 4);
+    if (tiers.size() > 1 && pilot >= 64) {
+        int64_t ovf = 0;
+        Status ps = run_tier(tiers.back(), pilot, nullptr, 0, &ovf);
+        if (ps.code) return ps;
+        if (ovf != 0) return fail(MCMI_ECUDA, "internal: pilot rows overflowed the last tier");
+        if (!e->h_pilot_buf(static_cast<size_t>(pilot))) return fail(MCMI_ENOMEM, "cudaMallocHost (pilot)");
+        MCMI_TRY(cudaMemcpyAsync(e->h_pilot, e->entries_before.p, pilot * sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, s),
+                 "read pilot");
+        MCMI_TRY(cudaStreamSynchronize(s), "read pilot");
+        // Start tier by a cost model over the pilot rows: a row of s distinct
+        // columns costs c_t on the tier that holds it and ~c_t * limit_t / s on
+        // each tier it overflows first (it aborts once the table is full).
+        // Relative costs c_t follow occupancy: smem <= 256: 1, smem 1024: 2,
+        // global: 3 (measured on the C5 grid, tools/c5_sweep.py).
+        auto tier_cost = [](const Tier& t) { return t.global ? 3.0 : (t.cap <= 256 ? 1.0 : 2.0); };
+        double best = 0.0;
+        for (size_t c0 = 0; c0 < tiers.size(); ++c0) {
+            double cost = 0.0;
+            for (int64_t i = 0; i < pilot; ++i) {
+                const double sr = static_cast<double>(std::max<int64_t>(1, e->h_pilot[i]));
+                for (size_t t = c0; t < tiers.size(); ++t) {
+                    if (tiers[t].cap_limit >= e->h_pilot[i] || t + 1 == tiers.size()) {
+                        cost += tier_cost(tiers[t]);
+                        break;
+                    }
+                    cost += tier_cost(tiers[t]) * std::min(1.0, tiers[t].cap_limit / sr);
+                }
+            }
+            if (c0 == 0 || cost < best) {
+                best = cost;
+                t0 = c0;
+            }
+        }
+        st.hash_cap = tiers[t0].cap;
+        offset = pilot;
+        work = rows - pilot;
+    }
+    const int* row_list = nullptr;
+    for (size_t ti = t0; ti < tiers.size() && work > 0; ++ti) {
+        int64_t overflowed = 0;
+        Status ts = run_tier(tiers[ti], work, row_list, row_list ? 0 : offset, &overflowed);
+        if (ts.code) return ts;
+        if (ti > t0) st.rows_retried += work;
         work = overflowed;
         row_list = e->ovf[cur].as<int>();
         cur ^= 1;

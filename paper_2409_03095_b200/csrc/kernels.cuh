@@ -66,7 +66,8 @@ struct TableBuildArgs {
 struct WalkArgs {
     Tables t;
     int64_t row_begin;      // global index of local row 0
-    const int* row_list;    // nullptr: work item i is row row_begin + i
+    const int* row_list;    // nullptr: work item i is row row_begin + work_offset + i
+    int64_t work_offset;
     int64_t n_work;
     int64_t n_chains, max_len;
     double delta;

@@ -371,7 +371,8 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
         if (lane == 0) wi = static_cast<long long>(atomicAdd(&a.counters[0], 1ull));
         wi = __shfl_sync(FULL_MASK, wi, 0);
         if (wi >= a.n_work) break;
-        const int64_t row = a.row_list ? static_cast<int64_t>(a.row_list[wi]) : a.row_begin + wi;
+        const int64_t row =
+            a.row_list ? static_cast<int64_t>(a.row_list[wi]) : a.row_begin + a.work_offset + wi;
         const int rowc = static_cast<int>(row);
 
         // the diagonal column's slot; its sum lives in a register (acc_r)

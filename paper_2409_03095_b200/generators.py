@@ -129,39 +129,33 @@ def powerlaw(n: int, gamma: float = 2.1, dmin: int = 2, dmax: int = 2000, seed: 
              lo: float = 1e-4, hi: float = 1.0) -> CsrMatrix:
     """Power-law row lengths (config C5, modelled on make_broad_spectrum,
     synthetic.cpp:162-191): deg ~ d^-gamma on [dmin, dmax], uniform random
-    columns, log-uniform |v| in [lo, hi], random sign, diag = 1.1*rowsum + 1."""
+    columns (duplicates merged, self-loops dropped), log-uniform |v| in
+    [lo, hi] with random sign (hash of (row, col)), diag = 1.1*rowsum + 1."""
     i = np.arange(n, dtype=np.uint64)
     base = np.uint64(seed) * np.uint64(0x100000001B3)
     u = _u01(i ^ base)
-    # inverse CDF of the continuous power law, floored
     a = 1.0 - gamma
-    d = ((dmax ** a - dmin ** a) * u + dmin ** a) ** (1.0 / a)
+    d = ((dmax ** a - dmin ** a) * u + dmin ** a) ** (1.0 / a)  # inverse CDF
     deg = np.clip(np.floor(d).astype(np.int64), dmin, dmax)
-    rp0 = np.zeros(n + 1, np.int64)
-    np.cumsum(deg, out=rp0[1:])
-    tot = int(rp0[-1])
     rows = np.repeat(np.arange(n, dtype=np.int64), deg)
-    e = np.arange(tot, dtype=np.uint64)
+    e = np.arange(rows.size, dtype=np.uint64)
     cols = (_u01(e * np.uint64(3) + base + np.uint64(1)) * n).astype(np.int64)
-    mag = np.exp(np.log(lo) + (np.log(hi) - np.log(lo)) * _u01(e * np.uint64(3) + base + np.uint64(2)))
-    sign = np.where(_u01(e * np.uint64(3) + base + np.uint64(3)) < 0.5, -1.0, 1.0)
-    keep = cols != rows
-    rows, cols, vals = rows[keep], cols[keep], (sign * mag)[keep]
-    order = np.lexsort((cols, rows))
-    rows, cols, vals = rows[order], cols[order], vals[order]
-    first = np.ones(rows.size, bool)
-    first[1:] = (rows[1:] != rows[:-1]) | (cols[1:] != cols[:-1])
-    rows, cols, vals = rows[first], cols[first], vals[first]  # drop duplicate columns
-    rowsum = np.zeros(n)
-    np.add.at(rowsum, rows, np.abs(vals))
-    diag_rows = np.arange(n, dtype=np.int64)
-    rows = np.concatenate([rows, diag_rows])
-    cols = np.concatenate([cols, diag_rows])
-    vals = np.concatenate([vals, 1.1 * rowsum + 1.0])
-    order = np.lexsort((cols, rows))
-    rows, cols, vals = rows[order], cols[order], vals[order]
+    key = np.sort(rows * n + cols)  # sorted by (row, col)
+    key = key[np.concatenate(([True], key[1:] != key[:-1]))]  # duplicates merged
+    rows, cols = key // n, key % n
+    off = cols != rows
+    key, rows, cols = key[off], rows[off], cols[off]
+    h = key.astype(np.uint64) ^ base
+    mag = np.exp(np.log(lo) + (np.log(hi) - np.log(lo)) * _u01(h * np.uint64(5) + np.uint64(7)))
+    vals = np.where(_u01(h * np.uint64(5) + np.uint64(9)) < 0.5, -mag, mag)
+    rowsum = np.bincount(rows, weights=np.abs(vals), minlength=n)
+    diag_key = np.arange(n, dtype=np.int64) * (n + 1)
+    pos = np.searchsorted(key, diag_key)
+    cols = np.insert(cols, pos, np.arange(n, dtype=np.int64))
+    vals = np.insert(vals, pos, 1.1 * rowsum + 1.0)
+    counts = np.bincount(rows, minlength=n) + 1
     rp = np.zeros(n + 1, np.int64)
-    np.cumsum(np.bincount(rows, minlength=n), out=rp[1:])
+    np.cumsum(counts, out=rp[1:])
     return CsrMatrix(n, rp, cols, vals)
 
 
@@ -173,4 +167,8 @@ CONFIGS = {
     "c3_lap3d_100": (lambda: laplacian3d(100), {}),
     "c3_lap3d_100_heavy": (lambda: laplacian3d(100), {"epsilon": 0.01, "delta": 0.01, "alpha": 1.5}),
     "c4_convdiff_1000": (lambda: convection_diffusion(1000), {}),
+    # C5: one point of the eps/delta sweep (tools/c5_sweep.py runs the grid)
+    "c5_powerlaw_4m": (lambda: powerlaw(4_000_000),
+                       {"alpha": 0.1, "delta": 1e-300, "chains_override": 100, "max_len_override": 8,
+                        "retain_k": 32}),
 }

@@ -181,14 +181,30 @@ def test_row_shards_concatenate_to_full(mc):
 
 @pytest.mark.parametrize("rng", [0, 1])
 def test_overflow_tier_retry(mc, oracle_mod, rng):
-    # long walks on a dense-ish random matrix force rows past the first
-    # accumulator tier; the retried rows must still be exact
+    # a 200-row shard (too small for the tier pilot) of rows touching up to
+    # ~1700 columns: rows overflow the first shared-memory tier and are re-run
+    # on larger tiers; the retried rows must still be exact
+    b = _csr(mc, "broad:1024:24:1e-4:1:7")
+    cfg = mc.McConfig(epsilon=.02, delta=.01, alpha=1.5, master_seed=42, rng_mode=rng)
+    inv = mc.compute_preconditioner(b, cfg, rows=(0, 200))
+    assert inv.stats["rows_retried"] > 0
+    want = oracle_mod.compute_preconditioner(b.n, b.row_ptr, b.col_idx, b.values, row_begin=0, row_end=200,
+                                             **cfg.oracle_kwargs())
+    assert np.array_equal(inv.m.row_ptr, want.row_ptr)
+    assert bits_equal(inv.m.values, want.values) and np.array_equal(inv.m.col_idx, want.col_idx)
+
+
+@pytest.mark.parametrize("rng", [0, 1])
+def test_tier_pilot_path_exact(mc, oracle_mod, rng):
+    # the full 1024 rows: the pilot builds rows [0, 256) on the last tier and
+    # picks the start tier for the rest; the result is tier-independent
     b = _csr(mc, "broad:1024:24:1e-4:1:7")
     cfg = mc.McConfig(epsilon=.02, delta=.01, alpha=1.5, master_seed=42, rng_mode=rng)
     inv = mc.compute_preconditioner(b, cfg)
-    assert inv.stats["rows_retried"] > 0
     want = oracle_mod.compute_preconditioner(b.n, b.row_ptr, b.col_idx, b.values, **cfg.oracle_kwargs())
+    assert np.array_equal(inv.m.row_ptr, want.row_ptr)
     assert bits_equal(inv.m.values, want.values) and np.array_equal(inv.m.col_idx, want.col_idx)
+    assert np.array_equal(inv.row_meta.entries_before_retention, want.entries_before)
 
 
 def test_keyed_within_mc_tolerance_of_reference(mc):
