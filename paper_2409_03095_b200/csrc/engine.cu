@@ -193,6 +193,12 @@ Status engine_init(mcmi_engine* e, int device) {
     MCMI_TRY(cudaMallocHost(&e->h_red, sizeof(Reductions)), "cudaMallocHost");
     MCMI_TRY(cudaMallocHost(&e->h_ctr, 8 * sizeof(unsigned long long)), "cudaMallocHost");
     MCMI_TRY(cudaMallocHost(&e->h_i64, 4 * sizeof(int64_t)), "cudaMallocHost");
+    // keep stream-ordered allocations (host-API input staging) cached in the pool
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
     return ok();
 }
 
@@ -285,8 +291,8 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     MCMI_TRY(e->a_cnt.ensure(n1 * sizeof(unsigned)), "alloc a_cnt");
     MCMI_TRY(e->a_off.ensure((n1 + 1) * sizeof(unsigned)), "alloc a_off");
     MCMI_TRY(e->rec.ensure(2 * n1 * sizeof(uint4)), "alloc rec");
-    MCMI_TRY(e->ent.ensure(z1 * sizeof(double2)), "alloc ent");
-    MCMI_TRY(e->colA.ensure(z1 * sizeof(int)), "alloc col");
+    MCMI_TRY(e->ent.ensure((z1 + 2) * sizeof(double2)), "alloc ent");  // +2: aligned pair loads
+    MCMI_TRY(e->colA.ensure((z1 + 2) * sizeof(int)), "alloc col");
     MCMI_TRY(e->b1.ensure(n1 * sizeof(double)), "alloc b1");
     MCMI_TRY(e->scan_tmp.ensure(scan_scratch_bytes(std::max(n1, z1)) + 64), "alloc scan");
 
@@ -601,12 +607,15 @@ struct mcmi_result {
     int64_t n = 0, nnz = 0;
     int64_t n_chains = 1, max_len = 1;
     mcmi_stats stats{};
-    // device arrays owned by the result
-    int64_t* rp = nullptr;
-    int64_t* ci = nullptr;
-    double* v = nullptr;
-    int64_t* cu = nullptr;
-    int64_t* eb = nullptr;
+    // The result keeps its engine checked out of the cache: the arrays below
+    // are the engine's own buffers (no per-call device allocation or free);
+    // mcmi_result_free returns the engine to the cache.
+    mcmi_engine* engine = nullptr;
+    const int64_t* rp = nullptr;
+    const int64_t* ci = nullptr;
+    const double* v = nullptr;
+    const int64_t* cu = nullptr;
+    const int64_t* eb = nullptr;
 };
 
 extern "C" {
@@ -693,22 +702,17 @@ int mcmi_build_rows(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_
         r->n_chains = stats.n_chains;
         r->max_len = stats.max_len;
         r->stats = stats;
-        // hand the engine's output buffers to the result (no device copy)
+        r->engine = e;
         r->rp = dc.row_ptr;
         r->ci = dc.col_idx;
         r->v = dc.values;
         r->cu = dc.chains_used;
         r->eb = dc.entries_before;
-        e->out_rp = DevBuf{};
-        e->out_col = DevBuf{};
-        e->out_val = DevBuf{};
-        e->chains_used = DevBuf{};
-        e->entries_before = DevBuf{};
         *out = r;
         return ok();
     };
     st = run();
-    release_engine(e);
+    if (st.code) release_engine(e);  // on success the result owns the engine until freed
     return report(st, err, errlen);
 }
 
@@ -724,15 +728,17 @@ int mcmi_result_copy(const mcmi_result* r, int64_t* row_ptr, int64_t* col_idx, d
                      int64_t* max_len) {
     if (!r) return MCMI_EINVAL;
     if (cudaSetDevice(r->device) != cudaSuccess) return MCMI_ECUDA;
+    cudaStream_t s = r->engine->own;
     cudaError_t e = cudaSuccess;
     auto cp = [&](void* dst, const void* src, size_t bytes) {
-        if (dst && src && bytes && e == cudaSuccess) e = cudaMemcpy(dst, src, bytes, cudaMemcpyDefault);
+        if (dst && src && bytes && e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s);
     };
-    cp(row_ptr, r->rp, (r->n + 1) * sizeof(int64_t));
-    cp(col_idx, r->ci, r->nnz * sizeof(int64_t));
+    cp(col_idx, r->ci, r->nnz * sizeof(int64_t));  // largest first
     cp(values, r->v, r->nnz * sizeof(double));
+    cp(row_ptr, r->rp, (r->n + 1) * sizeof(int64_t));
     cp(chains_used, r->cu, r->n * sizeof(int64_t));
     cp(entries_before, r->eb, r->n * sizeof(int64_t));
+    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
     if (n_chains) *n_chains = r->n_chains;
     if (max_len) *max_len = r->max_len;
     return e == cudaSuccess ? MCMI_OK : MCMI_ECUDA;
@@ -746,12 +752,7 @@ int mcmi_result_stats(const mcmi_result* r, mcmi_stats* stats) {
 
 void mcmi_result_free(mcmi_result* r) {
     if (!r) return;
-    cudaSetDevice(r->device);
-    cudaFree(r->rp);
-    cudaFree(r->ci);
-    cudaFree(r->v);
-    cudaFree(r->cu);
-    cudaFree(r->eb);
+    if (r->engine) release_engine(r->engine);
     delete r;
 }
 

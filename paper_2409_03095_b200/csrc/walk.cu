@@ -71,6 +71,15 @@ __device__ __forceinline__ WarpSmem carve(unsigned char* base, int cap, int logn
     return s;
 }
 
+// 256-bit read-only global load (LDG.E.ENL2.256 on sm_100a): a whole 32-byte
+// state record in one instruction.
+__device__ __forceinline__ void ldg256(const void* p, uint4& lo, uint4& hi) {
+    asm volatile("ld.global.nc.v8.u32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(lo.x), "=r"(lo.y), "=r"(lo.z), "=r"(lo.w), "=r"(hi.x), "=r"(hi.y), "=r"(hi.z),
+                   "=r"(hi.w)
+                 : "l"(p));
+}
+
 // Insert-or-find; returns the slot or -1 if the table is full.
 __device__ __forceinline__ int hash_slot(int* keys, unsigned mask, int shift, int col,
                                          int& n_new) {
@@ -420,7 +429,8 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             for (int64_t t = 0; __any_sync(FULL_MASK, alive); ++t) {
                 if (alive && t >= L) alive = false;
                 if (!alive) continue;
-                const uint4 r0 = rec[2 * static_cast<int64_t>(state)];
+                uint4 r0, r1;
+                ldg256(rec + 2 * static_cast<int64_t>(state), r0, r1);
                 const unsigned deg = r0.y;
                 if (deg == 0) {  // absorbing state (mc_engine.cpp:68)
                     alive = false;
@@ -432,9 +442,8 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 int nxt;
                 if (deg == 1) {  // forced move, no draw (mc_engine.cpp:69); inline in the record
                     ratio = __hiloint2double(static_cast<int>(r0.w), static_cast<int>(r0.z));
-                    nxt = static_cast<int>(rec[2 * static_cast<int64_t>(state) + 1].z);
+                    nxt = static_cast<int>(r1.z);
                 } else {
-                    const uint4 r1 = rec[2 * static_cast<int64_t>(state) + 1];
                     double u;
                     if (MODE == 0) {
                         const unsigned long long b = pos >> 1;
