@@ -78,7 +78,7 @@ struct WalkArgs {
     int cap_limit;          // max distinct columns before the row overflows to the next tier
     int lanes;              // chains per batch (<= 32)
     int log_stride;         // max(max_len, 1) step deposits per chain
-    unsigned log_magic;     // ceil(2^32 / log_stride): p / log_stride == __umulhi(p, log_magic)
+    unsigned log_magic;     // ceil(2^32 / log_stride) for log_stride >= 2: p / S == __umulhi(p, magic)
     int ell0;               // initial speculative draw stride (reference-stream mode)
     unsigned char* gscratch;  // global-tier per-warp accumulator + log (nullptr for smem tiers)
     // outputs, indexed by local row (row - row_begin)

@@ -413,8 +413,10 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 chain = chains_done + lane;
                 active = lane < B && chain < N;
             }
-            int* lc = sm.log_col + lane * S;
-            double* lw = sm.log_w + lane * S;
+            // step-major log: deposit t of chain (lane) at [t * B + lane], so the
+            // walk's writes are bank-conflict free; the fold reads chain-major
+            int* lc = sm.log_col + lane;
+            double* lw = sm.log_w + lane;
             int m = 0;              // step deposits logged (W0 = 1 at (r, r) is implicit)
             unsigned retm = 0;      // bit t: step deposit t went back to column r (t < 32)
             bool ret_hi = false;    // a return at t >= 32
@@ -504,8 +506,8 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 }
                 w *= ratio;  // w *= a_k / p_k (mc_engine.cpp:94)
                 state = nxt;
-                lc[m] = state;
-                lw[m] = w;
+                lc[m * B] = state;
+                lw[m * B] = w;
                 ++m;
                 if (state == rowc) {
                     if (retm == 0 && !ret_hi) ret_w = w;
@@ -516,7 +518,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             }
 
             if (active)
-                for (int t1 = m; t1 < S; ++t1) lc[t1] = -1;  // end-of-chain sentinel for the fold
+                for (int t1 = m; t1 < S; ++t1) lc[t1 * B] = -1;  // end-of-chain sentinel for the fold
 
             // ------------------------------------------- which lanes count
             unsigned valid;
@@ -528,6 +530,8 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 valid = 1u;
                 chains_run = 1;
                 row_done = true;
+            } else if (MODE == 0 && __all_sync(FULL_MASK, !active || draws == ell)) {
+                valid = __ballot_sync(FULL_MASK, active);  // every chain drew ell times: all on the orbit
             } else if (MODE == 0) {
                 int nxtl = lane;
                 if (active && draws > 0) {
@@ -590,15 +594,15 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                             while (rest) {
                                 const int t1 = __ffs(rest) - 1;
                                 rest &= rest - 1;
-                                acc_r += sm.log_w[j * S + t1];
+                                acc_r += sm.log_w[t1 * B + j];
                             }
                             if (hi) {  // returns at steps >= 32 (max_len > 32 only)
                                 bool skip = rm == 0;  // the first return was at a step >= 32
                                 const int mj = __shfl_sync(FULL_MASK, m, j);
                                 for (int t1 = 32; t1 < mj; ++t1)
-                                    if (sm.log_col[j * S + t1] == rowc) {
+                                    if (sm.log_col[t1 * B + j] == rowc) {
                                         if (skip) skip = false;
-                                        else acc_r += sm.log_w[j * S + t1];
+                                        else acc_r += sm.log_w[t1 * B + j];
                                     }
                             }
                         }
@@ -616,9 +620,11 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             const int span = B * S;
             for (int base = 0; base < span; base += 32) {
                 const int p = base + lane;
-                const int j = min(static_cast<int>(__umulhi(static_cast<unsigned>(p), a.log_magic)), 31);
+                // chain of position p: p / S (S == 1: the magic would be 2^32)
+                const int j = min(S == 1 ? p : static_cast<int>(__umulhi(static_cast<unsigned>(p), a.log_magic)), 31);
                 bool ok = p < span && ((valid >> j) & 1u);
-                int c = ok ? sm.log_col[p] : -1;
+                const int q = (p - j * S) * B + j;  // chain-major position p -> step-major slot
+                int c = ok ? sm.log_col[q] : -1;
                 ok = ok && c >= 0 && c != rowc;  // column r was folded in (i)
                 if (!ok) c = -1 - lane;          // unique non-column tag
                 const unsigned peers = __match_any_sync(FULL_MASK, c);
@@ -636,7 +642,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                     if (slot < 0) fail = true;
                 }
                 slot = __shfl_sync(FULL_MASK, slot, leader);
-                const double w = ok ? sm.log_w[p] : 0.0;
+                const double w = ok ? sm.log_w[q] : 0.0;
                 double v = w;
                 if (ok && rank == 0 && slot >= 0) v = sm.vals[slot] + w;
                 const int maxsize = __reduce_max_sync(FULL_MASK, static_cast<unsigned>(gsize));

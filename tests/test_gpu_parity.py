@@ -309,3 +309,18 @@ def golden_input_tridiag(n):
     from paper_2409_03095_b200 import generators as G
     t = G.tridiagonal(n)
     return t.row_ptr, t.col_idx, t.values
+
+
+@pytest.mark.parametrize("rng", [0, 1])
+@pytest.mark.parametrize("max_len", [1, 3])
+def test_short_walk_lengths(mc, oracle_mod, ref_mod, rng, max_len):
+    # max_len 1 (one deposit per chain) and 3 (a log stride that does not divide 32)
+    b = _csr(mc, "ddm:64:0.2:11")
+    cfg = mc.McConfig(epsilon=.05, delta=1e-9, alpha=1.5, max_len_override=max_len, master_seed=5, rng_mode=rng)
+    inv = mc.compute_preconditioner(b, cfg)
+    want = oracle_mod.compute_preconditioner(b.n, b.row_ptr, b.col_idx, b.values, **cfg.oracle_kwargs())
+    assert np.array_equal(inv.m.col_idx, want.col_idx) and bits_equal(inv.m.values, want.values)
+    if rng == 0:
+        ref = ref_mod.compute_preconditioner(ref_mod.Csr(b.n, b.row_ptr, b.col_idx, b.values),
+                                             **{k: v for k, v in cfg.oracle_kwargs().items() if k != "rng_mode"})
+        assert bits_equal(inv.m.values, ref.m.values)
