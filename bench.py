@@ -343,6 +343,11 @@ def run_ours(args):
         except OSError:
             pass
         peak = float(peaks.get("hbm_gbs", 6650.0))
+        try:
+            with open(os.path.join(REPO, "profiles", "l2_peak.json")) as f:
+                l2_peak = float(json.load(f)["l2_read_gbs"])
+        except (OSError, ValueError, KeyError):
+            l2_peak = None
         walk_ms = float(mx[2])
         achieved = float(agg[3]) / (float(agg[2]) / 1e3) / 1e9 if float(agg[2]) > 0 else 0.0
         s0 = stats[-1]
@@ -359,7 +364,10 @@ def run_ours(args):
                           "walk_kernel": s0["ms_walk_kernel"]},
             "roofline": {"bound": "hbm", "kernel": "k_walk", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": load_traffic(args.config, args.rng),
-                         "bytes_per_step": "20 + 8*deg(s)", "walk_ms": walk_ms},
+                         "bytes_per_step": "20 + 8*deg(s)", "walk_ms": walk_ms,
+                         "l2_peak": l2_peak, "frac_l2": (achieved / l2_peak) if l2_peak else None,
+                         "note": "tables are L2-resident: frac_l2 is the binding roofline (L2 read peak "
+                                 "measured by tools/l2_peak.cu); traffic = DRAM bytes per walk launch (ncu)"},
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(sm[4]),
             "clocks": clk.summary(),
         }

@@ -49,7 +49,7 @@
 
 namespace mcmi {
 
-constexpr int kDefaultMinBlocks = 5;
+constexpr int kDefaultMinBlocks = 6;
 
 namespace {
 
