@@ -142,7 +142,6 @@ __device__ __forceinline__ Keep make_keep(const TableBuildArgs& a) {
 // off_diagonal_range (csr.cpp:88-105).
 __global__ void k_offdiag_range(TableBuildArgs a) {
     double mn = __longlong_as_double(0x7ff0000000000000ll), mx = 0.0;
-    bool seen = false;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
          i += (int64_t)gridDim.x * blockDim.x) {
         for (int64_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
@@ -150,10 +149,9 @@ __global__ void k_offdiag_range(TableBuildArgs a) {
             const double v = fabs(a.values[k]);
             mn = fmin(mn, v);
             mx = fmax(mx, v);
-            seen = true;
         }
     }
-    (void)seen;  // an unseen thread contributes (+inf, 0), the identities
+    // a thread that saw no off-diagonal contributes (+inf, 0), the identities
     mn = block_min(mn);
     mx = block_max(mx);
     if (threadIdx.x == 0 && mx >= mn) {  // block saw at least one off-diagonal
