@@ -563,7 +563,20 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 const int lv = 31 - __clz(valid);
                 const unsigned klv = __shfl_sync(FULL_MASK, draws, lv);
                 D = D + static_cast<unsigned long long>(lv) * ell + klv;
-                ell = draws0 > 0 ? draws0 : 1u;
+                // Next stride: prefix speculation (ell = chain 0's draws) yields
+                // ~1/p chains per window when a fraction p of chains draw a
+                // different count; dense candidates (ell = 1, every draw index)
+                // yield B/k.  Go dense when the prefix under-delivers, back to
+                // prefix once a dense window shows uniform draw counts.
+                const int nv = __popc(valid);
+                if (ell > 1 && nv * static_cast<int>(ell) < B) {
+                    ell = 1u;
+                } else if (ell == 1u) {
+                    const bool uniform = __all_sync(FULL_MASK, !((valid >> lane) & 1u) || draws == draws0);
+                    if (uniform && draws0 > 1) ell = draws0;
+                } else {
+                    ell = draws0 > 0 ? draws0 : 1u;
+                }
             }
             __syncwarp();
 
