@@ -219,7 +219,9 @@ void engine_release(mcmi_engine* e) {
     if (e->h_pilot) cudaFreeHost(e->h_pilot);
 }
 
-constexpr int kLogMax = 256;  // deposit-log entries per warp (shared memory)
+constexpr int kLogMax = 256;         // deposit-log entries per warp (shared memory)
+constexpr int64_t kMaxWalkLen = 1 << 16;  // longest walk (log capacity of the global tier)
+constexpr int64_t kMaxSmemWalkLen = 1024; // longer walks go straight to the global tier
 
 struct Tier {
     int cap, cap_limit, lanes, log_stride, warps_per_block;
@@ -246,8 +248,8 @@ Tier make_global_tier(int64_t bound, int64_t max_len) {
     while (cap - cap / 4 < bound && cap < (int64_t{1} << 30)) cap <<= 1;
     t.cap = static_cast<int>(cap);
     t.cap_limit = t.cap - t.cap / 4;
-    t.log_stride = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, max_len), INT_MAX / 64));
-    t.lanes = 32;
+    t.log_stride = static_cast<int>(std::min<int64_t>(std::max<int64_t>(1, max_len), kMaxWalkLen));
+    t.lanes = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(32, (int64_t{1} << 16) / t.log_stride)));
     t.warps_per_block = 8;
     t.global = true;
     return t;
@@ -355,6 +357,10 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     int64_t N = 1, L = 1;
     Status bs = chain_budget(cfg, a_norm, &N, &L);
     if (bs.code) return bs;
+    if (N > INT_MAX) return fail(MCMI_EINVAL, "chain budget exceeds 2^31-1 chains per row");
+    if (L > kMaxWalkLen)
+        return fail(MCMI_EINVAL, "max_len above " + std::to_string(kMaxWalkLen) +
+                                     " is not supported by the B200 build (deposit log capacity)");
     st.n_chains = N;
     st.max_len = L;
     st.a_norm = a_norm;
@@ -374,10 +380,12 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     static const int kTierCaps[] = {256, 1024};  // larger rows: the global tier (32 warps/SM)
     int first_cap = static_cast<int>(std::min<int64_t>(256, std::max<int64_t>(32, next_pow2((bound * 4 + 2) / 3))));
     std::vector<Tier> tiers;
-    tiers.push_back(make_tier(first_cap, L));
-    for (int c : kTierCaps)
-        if (c > first_cap && (tiers.back().cap_limit < bound)) tiers.push_back(make_tier(c, L));
-    if (tiers.back().cap_limit < bound) tiers.push_back(make_global_tier(bound, L));
+    if (L <= kMaxSmemWalkLen) {
+        tiers.push_back(make_tier(first_cap, L));
+        for (int c : kTierCaps)
+            if (c > first_cap && (tiers.back().cap_limit < bound)) tiers.push_back(make_tier(c, L));
+    }
+    if (tiers.empty() || tiers.back().cap_limit < bound) tiers.push_back(make_global_tier(bound, L));
     st.hash_cap = first_cap;  // updated below if the pilot starts on a larger tier
 
     MCMI_TRY(e->row_cnt.ensure(std::max<int64_t>(rows, 1) * sizeof(int)), "alloc row_cnt");
@@ -429,7 +437,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         if (t.global) {
             size_t free_b = 0, total_b = 0;
             MCMI_TRY(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-            const size_t per_warp = walk_global_bytes_per_warp(t.cap, t.log_stride);
+            const size_t per_warp = walk_global_bytes_per_warp(t.cap, t.lanes, t.log_stride);
             const size_t budget = std::min<size_t>(size_t{16} << 30, free_b / 2);
             max_warps = std::min<int64_t>(static_cast<int64_t>(budget / per_warp),
                                           static_cast<int64_t>(e->num_sms) * 32);

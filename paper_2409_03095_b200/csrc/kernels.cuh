@@ -101,7 +101,7 @@ cudaError_t launch_count_quantile(const TableBuildArgs& a, int64_t nnz, int64_t 
                                   void* scratch, size_t scratch_bytes, cudaStream_t s);
 size_t count_quantile_scratch_bytes(int64_t nnz);
 size_t walk_smem_bytes_per_warp(int cap, int lanes, int log_stride);
-size_t walk_global_bytes_per_warp(int cap, int log_stride);
+size_t walk_global_bytes_per_warp(int cap, int lanes, int log_stride);
 cudaError_t launch_walk(const WalkArgs& a, int warps_per_block, int num_sms, bool global_tier,
                         int64_t max_warps, cudaStream_t s);
 

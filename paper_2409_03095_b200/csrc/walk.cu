@@ -363,8 +363,9 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     const double2* __restrict__ ent = a.t.ent;
     const int* __restrict__ tcol = a.t.col;
     const uint2 key = make_uint2(static_cast<uint32_t>(a.seed), static_cast<uint32_t>(a.seed >> 32));
-    const int64_t N = a.n_chains;
-    const int64_t L = a.max_len;
+    // host guarantees 1 <= N < 2^31 and L < 2^31 (engine.cu), so 32-bit loop state
+    const int N = static_cast<int>(a.n_chains);
+    const int L = static_cast<int>(a.max_len);
 
     unsigned long long tot_steps = 0, tot_deg = 0;
 
@@ -376,12 +377,11 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     __syncwarp();
 
     for (;;) {
-        long long wi = 0;
-        if (lane == 0) wi = static_cast<long long>(atomicAdd(&a.counters[0], 1ull));
+        int wi = 0;
+        if (lane == 0) wi = static_cast<int>(atomicAdd(&a.counters[0], 1ull));
         wi = __shfl_sync(FULL_MASK, wi, 0);
         if (wi >= a.n_work) break;
-        const int64_t row =
-            a.row_list ? static_cast<int64_t>(a.row_list[wi]) : a.row_begin + a.work_offset + wi;
+        const int row = a.row_list ? a.row_list[wi] : static_cast<int>(a.row_begin + a.work_offset) + wi;
         const int rowc = static_cast<int>(row);
 
         // the diagonal column's slot; its sum lives in a register (acc_r)
@@ -393,8 +393,8 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
 
         int distinct = 1;
         bool overflow = false;
-        int64_t chains_done = 0;
-        int64_t chains_run = N;
+        int chains_done = 0;
+        int chains_run = N;
         unsigned long long row_steps = 0, row_deg = 0;
         // reference-stream speculation state
         unsigned long long D = 0;
@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             // ------------------------------------------------ walk one batch
             bool active;
             unsigned long long pos = 0;  // next draw index (reference stream)
-            int64_t chain = 0;           // chain index (keyed)
+            int chain = 0;               // chain index (keyed)
             if (MODE == 0) {
                 active = lane < B;
                 pos = D + static_cast<unsigned long long>(lane) * ell;
@@ -428,7 +428,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             unsigned long long cached = ~0ull;
             uint4 blk = make_uint4(0, 0, 0, 0);
             bool alive = active;
-            for (int64_t t = 0; __any_sync(FULL_MASK, alive); ++t) {
+            for (int t = 0; __any_sync(FULL_MASK, alive); ++t) {
                 if (alive && t >= L) alive = false;
                 if (!alive) continue;
                 uint4 r0, r1;
@@ -453,7 +453,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                             blk = philox4x32_10(
                                 make_uint4(static_cast<uint32_t>(b), static_cast<uint32_t>(b >> 32),
                                            static_cast<uint32_t>(row),
-                                           static_cast<uint32_t>(static_cast<uint64_t>(row) >> 32)),
+                                           0u),  // row < 2^31: stream id high word
                                 key);
                             cached = b;
                         }
@@ -461,12 +461,12 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                                       : u32pair_to_double(blk.x, blk.y);
                         ++pos;
                     } else {
-                        const unsigned long long b = static_cast<unsigned long long>(t) >> 1;
+                        const unsigned long long b = static_cast<unsigned>(t) >> 1;
                         if (b != cached) {
                             blk = philox4x32_10(
                                 make_uint4(static_cast<uint32_t>(b), static_cast<uint32_t>(chain),
                                            static_cast<uint32_t>(row),
-                                           static_cast<uint32_t>(static_cast<uint64_t>(row) >> 32)),
+                                           0u),  // row < 2^31: stream id high word
                                 key);
                             cached = b;
                         }
@@ -552,7 +552,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             } else {
                 valid = __ballot_sync(FULL_MASK, active);
             }
-            const int64_t remaining = N - chains_done;
+            const int remaining = N - chains_done;
             if (remaining < 32) valid = lowest_bits(valid, static_cast<int>(remaining));
             const bool mine = (valid >> lane) & 1u;
             if (mine) {
@@ -675,7 +675,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             if (chains_done >= N) row_done = true;
         }
 
-        const int64_t lrow = row - a.row_begin;
+        const int64_t lrow = static_cast<int64_t>(row) - a.row_begin;
         if (overflow) {
             if (lane == 0) {
                 const unsigned long long q = atomicAdd(&a.counters[3], 1ull);
@@ -761,7 +761,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             touched = max(touched, sort_by_column(sm.keys, sm.vals, s));
         }
 
-        const int64_t out_off = a.stage_base + wi * a.stage_stride;
+        const int64_t out_off = a.stage_base + static_cast<int64_t>(wi) * a.stage_stride;
         int* __restrict__ oc = a.stage_col + out_off;
         double* __restrict__ ov = a.stage_val + out_off;
         int n_out = 0;
@@ -819,8 +819,8 @@ size_t walk_smem_bytes_per_warp(int cap, int lanes, int log_stride) {
     return static_cast<size_t>(cap + round32(lanes * log_stride)) * 12;
 }
 
-size_t walk_global_bytes_per_warp(int cap, int log_stride) {
-    return walk_smem_bytes_per_warp(cap, 32, log_stride);
+size_t walk_global_bytes_per_warp(int cap, int lanes, int log_stride) {
+    return walk_smem_bytes_per_warp(cap, lanes, log_stride);
 }
 
 template <int MODE, int MINB, bool GL>
