@@ -302,9 +302,22 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     init.offmin_bits = 0x7ff0000000000000ull;
     init.degenerate_row = LLONG_MAX;
     init.bad_col_row = LLONG_MAX;
+    init.bad_rowptr_row = LLONG_MAX;
     *e->h_red = init;
     MCMI_TRY(cudaMemcpyAsync(e->red.p, e->h_red, sizeof(Reductions), cudaMemcpyHostToDevice, s),
              "init reductions");
+
+    // row_ptr must be a valid CSR row pointer before any column is read
+    if (n > 0) {
+        MCMI_TRY(launch_validate_row_ptr(b.row_ptr, n, nnz, e->red.as<Reductions>(), s), "validate row_ptr");
+        MCMI_TRY(cudaMemcpyAsync(e->h_red, e->red.p, sizeof(Reductions), cudaMemcpyDeviceToHost, s),
+                 "read validation");
+        MCMI_TRY(cudaStreamSynchronize(s), "validate row_ptr");
+        if (e->h_red->bad_rowptr_row != LLONG_MAX)
+            return fail(MCMI_EINVAL, "row_ptr is not a valid CSR row pointer at row " +
+                                         std::to_string(e->h_red->bad_rowptr_row));
+        st.launches += 1;
+    }
 
     TableBuildArgs ta{};
     ta.n = n;

@@ -18,7 +18,8 @@ struct Reductions {
     unsigned long long a_nnz;        // entries of A
     unsigned long long cq_threshold_bits;  // count-quantile: |v| of the n_drop-th smallest
     long long cq_tie_budget;               // count-quantile: ties at the threshold to drop
-    unsigned long long pad[6];
+    long long bad_rowptr_row;              // first row with an invalid row_ptr, else LLONG_MAX
+    unsigned long long pad[5];
 };
 
 // Transition tables (subsystem 1), one 32-byte record per state s:
@@ -94,6 +95,8 @@ struct WalkArgs {
     int* overflow_list;
 };
 
+cudaError_t launch_validate_row_ptr(const int64_t* row_ptr, int64_t n, int64_t nnz, Reductions* red,
+                                   cudaStream_t s);
 cudaError_t launch_table_build(const TableBuildArgs& a, int64_t nnz, bool drop_active,
                                cudaStream_t s);
 cudaError_t launch_table_fill(const TableBuildArgs& a, cudaStream_t s);

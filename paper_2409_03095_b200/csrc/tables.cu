@@ -139,6 +139,18 @@ __device__ __forceinline__ Keep make_keep(const TableBuildArgs& a) {
     return kp;
 }
 
+// CSR sanity before any column is read: row_ptr[0] == 0, non-decreasing,
+// row_ptr[n] == nnz.  The first offending row lands in bad_rowptr_row.
+__global__ void k_validate_row_ptr(const int64_t* __restrict__ rp, int64_t n, int64_t nnz,
+                                   Reductions* red) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t a = rp[i], b = rp[i + 1];
+        if (a > b || a < 0 || b > nnz || (i == 0 && a != 0))
+            atomicMin(&red->bad_rowptr_row, static_cast<long long>(i));
+    }
+}
+
 // off_diagonal_range (csr.cpp:88-105).
 __global__ void k_offdiag_range(TableBuildArgs a) {
     double mn = __longlong_as_double(0x7ff0000000000000ll), mx = 0.0;
@@ -421,6 +433,12 @@ cudaError_t launch_count_quantile(const TableBuildArgs& a, int64_t nnz, int64_t 
     cudaError_t e = scan_u32_exclusive(tie, tie_rank, nnz, scan_tmp, s);
     if (e != cudaSuccess) return e;
     k_cq_keep<<<g, TB, 0, s>>>(a, st, tie_rank);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_validate_row_ptr(const int64_t* row_ptr, int64_t n, int64_t nnz, Reductions* red,
+                                   cudaStream_t s) {
+    if (n > 0) k_validate_row_ptr<<<grid_for(n), TB, 0, s>>>(row_ptr, n, nnz, red);
     return cudaGetLastError();
 }
 

@@ -218,6 +218,9 @@ def compute_preconditioner(b: CsrMatrix, cfg: McConfig | None = None, n_threads:
     """
     del n_threads
     cfg = cfg or McConfig()
+    if b.row_ptr.size != b.n + 1 or (b.n > 0 and (b.col_idx.size < b.row_ptr[-1] or b.values.size < b.row_ptr[-1])):
+        raise ValueError("CsrMatrix arrays are inconsistent with row_ptr (need n+1 row pointers and "
+                         "row_ptr[n] column indices and values)")
     lib = L.load()
     view = L.mcmi_csr_view(int(b.n), b.row_ptr.ctypes.data, b.col_idx.ctypes.data if b.col_idx.size else None,
                            b.values.ctypes.data if b.values.size else None)

@@ -324,3 +324,15 @@ def test_short_walk_lengths(mc, oracle_mod, ref_mod, rng, max_len):
         ref = ref_mod.compute_preconditioner(ref_mod.Csr(b.n, b.row_ptr, b.col_idx, b.values),
                                              **{k: v for k, v in cfg.oracle_kwargs().items() if k != "rng_mode"})
         assert bits_equal(inv.m.values, ref.m.values)
+
+
+def test_invalid_row_ptr_rejected_without_fault(mc):
+    # a decreasing row_ptr and one pointing past nnz must be rejected before any
+    # column is read (the reference has undefined behaviour here)
+    for rp in ([0, 2, 1, 3], [0, 1, 4, 3], [1, 1, 2, 3]):
+        bad = mc.CsrMatrix(3, np.array(rp), np.array([0, 1, 2]), np.array([1.0, 1.0, 1.0]))
+        with pytest.raises(ValueError, match="row_ptr"):
+            mc.compute_preconditioner(bad, mc.McConfig())
+    # the device is still healthy afterwards
+    ok = mc.compute_preconditioner(mc.CsrMatrix.identity(4), mc.McConfig(alpha=1.0))
+    assert ok.m.nnz() == 4
