@@ -155,6 +155,37 @@ int mcmi_engine_build(mcmi_engine* e, const mcmi_csr_view* b_dev, const mcmi_con
                       int64_t row_begin, int64_t row_end, void* stream, mcmi_device_csr* out,
                       mcmi_stats* stats, char* err, size_t errlen);
 
+/* ------------------------------------------------- consumer of M (§8f) */
+
+/* SolverMethod / SolverConfig (solvers.hpp:11-18) */
+#define MCMI_SOLVER_GMRES 0
+#define MCMI_SOLVER_BICGSTAB 1
+
+typedef struct mcmi_solver_config {
+    int32_t method;   /* MCMI_SOLVER_*, default gmres */
+    int32_t reserved;
+    double rel_tol;   /* default 1e-6 */
+    int64_t max_iters; /* default 30000 */
+    int64_t restart;  /* GMRES only, default 50 */
+} mcmi_solver_config;
+
+/* SolveReport (solvers.hpp:20-30), without the history and x (x is an output buffer) */
+typedef struct mcmi_solve_report {
+    int32_t converged;
+    int32_t breakdown;
+    int64_t iterations;
+    double final_rel_residual; /* true residual ||rhs - B x|| / ||rhs|| */
+    double ms;                 /* device time */
+} mcmi_solve_report;
+
+void mcmi_solver_config_default(mcmi_solver_config* cfg);
+/* Left-preconditioned GMRES / BiCGstab on device-resident B and M (M NULL =
+ * unpreconditioned), mirroring solvers.cpp:54-238; rhs NULL means B * ones
+ * (ones_product_rhs).  x: device buffer of n doubles (solution, x0 = 0). */
+int mcmi_solve_device(const mcmi_csr_view* b_dev, const mcmi_csr_view* m_dev, const double* rhs_dev,
+                      double* x_dev, const mcmi_solver_config* cfg, int device, void* stream,
+                      mcmi_solve_report* rep, char* err, size_t errlen);
+
 /* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream): copies an
  * engine output into caller-owned host or device memory. */
 int mcmi_copy(void* dst, const void* src, size_t bytes, void* stream);

@@ -19,7 +19,7 @@ MCMI_OK, MCMI_EINVAL, MCMI_ESPLIT, MCMI_ERANGE, MCMI_ECUDA, MCMI_ENOMEM, MCMI_EN
 EXPORTS = [
     "mcmi_config_default", "mcmi_build", "mcmi_build_rows", "mcmi_result_sizes", "mcmi_result_copy",
     "mcmi_result_stats", "mcmi_result_free", "mcmi_engine_create", "mcmi_engine_destroy",
-    "mcmi_engine_build", "mcmi_copy", "mcmi_version",
+    "mcmi_engine_build", "mcmi_copy", "mcmi_version", "mcmi_solver_config_default", "mcmi_solve_device",
 ]
 
 
@@ -82,6 +82,16 @@ class mcmi_device_csr(C.Structure):
     ]
 
 
+class mcmi_solver_config(C.Structure):
+    _fields_ = [("method", C.c_int32), ("reserved", C.c_int32), ("rel_tol", C.c_double),
+                ("max_iters", C.c_int64), ("restart", C.c_int64)]
+
+
+class mcmi_solve_report(C.Structure):
+    _fields_ = [("converged", C.c_int32), ("breakdown", C.c_int32), ("iterations", C.c_int64),
+                ("final_rel_residual", C.c_double), ("ms", C.c_double)]
+
+
 _lib = None
 
 
@@ -115,5 +125,10 @@ def load(path: str | None = None):
                                     C.c_char_p, C.c_size_t]
     L.mcmi_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
     L.mcmi_version.restype = C.c_char_p
+    L.mcmi_solver_config_default.argtypes = [C.POINTER(mcmi_solver_config)]
+    L.mcmi_solver_config_default.restype = None
+    L.mcmi_solve_device.argtypes = [C.POINTER(mcmi_csr_view), C.POINTER(mcmi_csr_view), C.c_void_p, C.c_void_p,
+                                    C.POINTER(mcmi_solver_config), C.c_int, C.c_void_p,
+                                    C.POINTER(mcmi_solve_report), C.c_char_p, C.c_size_t]
     _lib = L
     return L

@@ -2,7 +2,11 @@
 #pragma once
 
 #include <cstdint>
+#include <string>
+
 #include <cuda_runtime.h>
+
+#include "../../include/mcmi.h"
 
 namespace mcmi {
 
@@ -117,5 +121,9 @@ cudaError_t scan_rows_exclusive(const int* in, int64_t* out, int64_t n, void* sc
 cudaError_t launch_compact(const int* stage_col, const double* stage_val, const int64_t* row_src,
                            const int* row_cnt, const int64_t* row_ptr, int64_t rows,
                            int64_t* col_out, double* val_out, cudaStream_t s);
+
+// Validation solvers on device (solver.cu).
+int solve_device(const mcmi_csr_view& b, const mcmi_csr_view* m, const double* rhs, double* x,
+                 const mcmi_solver_config& cfg, cudaStream_t s, mcmi_solve_report* rep, std::string& msg);
 
 }  // namespace mcmi

@@ -1,0 +1,410 @@
+// solver.cu — SURVEY.md §8(f) rank 1: the consumer of M on the GPU.
+//
+// Left-preconditioned restarted GMRES (MGS Arnoldi + Givens) and BiCGstab,
+// step for step as the reference's validation solvers
+// (/root/reference/proj/src/solvers.cpp:54-238): same x0 = 0, same
+// preconditioned residual recurrences, same breakdown thresholds, same
+// true-residual convergence contract (||rhs - B x|| / ||rhs|| <= rel_tol).
+//
+// Arithmetic: each SpMV row is a sequential sum in stored order and every
+// axpy/scale is elementwise, so those round exactly like the reference
+// (-fmad=false).  Dot products are deterministic two-level tree reductions
+// (fixed launch shape), not the reference's sequential loop, so iterates drift
+// at the rounding level and iteration counts agree within a small delta
+// (tests/test_gpu_solver.py states it).
+#include <cmath>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/mcmi.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace mcmi {
+namespace {
+
+constexpr int ST = 256;
+constexpr int kDotBlocks = 148 * 4;
+
+struct DevCsr {
+    int64_t n;
+    const int64_t* rp;
+    const int64_t* ci;
+    const double* v;
+};
+
+// y = m * x (csr.cpp:159-170): one thread per row, sequential in stored order.
+__global__ void k_spmv(DevCsr m, const double* __restrict__ x, double* __restrict__ y) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int64_t k = m.rp[i]; k < m.rp[i + 1]; ++k) s += m.v[k] * x[m.ci[k]];
+        y[i] = s;
+    }
+}
+
+// partial[b] = sum over the block's grid-stride slice of a[i]*b[i]
+__global__ void k_dot_partial(const double* __restrict__ a, const double* __restrict__ b, int64_t n,
+                              double* __restrict__ partial) {
+    __shared__ double red[ST / 32];
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        s += a[i] * b[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL_MASK, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < ST / 32; ++w) t += red[w];
+        partial[blockIdx.x] = t;
+    }
+}
+
+__global__ void k_dot_final(const double* __restrict__ partial, int nb, double* __restrict__ out) {
+    __shared__ double red[ST / 32];
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) s += partial[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL_MASK, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < ST / 32; ++w) t += red[w];
+        *out = t;
+    }
+}
+
+// y += a * x  (solvers.cpp:19-21)
+__global__ void k_axpy(double a, const double* __restrict__ x, double* __restrict__ y, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] += a * x[i];
+}
+
+// y = x / d
+__global__ void k_div(const double* __restrict__ x, double d, double* __restrict__ y, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = x[i] / d;
+}
+
+// r = a - b
+__global__ void k_sub(const double* __restrict__ a, const double* __restrict__ b, double* __restrict__ r,
+                      int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        r[i] = a[i] - b[i];
+}
+
+// p = r + beta * (p - omega * v)   (solvers.cpp:198-199)
+__global__ void k_bicg_p(const double* __restrict__ r, double beta, double omega, const double* __restrict__ v,
+                         double* __restrict__ p, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        p[i] = r[i] + beta * (p[i] - omega * v[i]);
+}
+
+__global__ void k_fill(double* __restrict__ y, double v, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = v;
+}
+
+inline unsigned grid_n(int64_t n) {
+    int64_t g = (n + ST - 1) / ST;
+    if (g < 1) g = 1;
+    if (g > 148 * 8) g = 148 * 8;
+    return static_cast<unsigned>(g);
+}
+
+struct Ctx {
+    cudaStream_t s;
+    int64_t n;
+    DevCsr b;
+    DevCsr m;
+    bool prec;
+    double* partial;  // [kDotBlocks]
+    double* scal;     // device scalar
+    double* h_scal;   // pinned
+    std::vector<double*> owned;
+    cudaError_t err = cudaSuccess;
+
+    double* vec() {
+        double* p = nullptr;
+        if (err == cudaSuccess) err = cudaMallocAsync(&p, static_cast<size_t>(n > 0 ? n : 1) * sizeof(double), s);
+        if (p) owned.push_back(p);
+        return p;
+    }
+    void spmv(const DevCsr& a, const double* x, double* y) { k_spmv<<<grid_n(n), ST, 0, s>>>(a, x, y); }
+    void op(const double* x, double* y, double* tmp) {  // y = M (B x)   (solvers.cpp:23-28)
+        if (prec) {
+            spmv(b, x, tmp);
+            spmv(m, tmp, y);
+        } else {
+            spmv(b, x, y);
+        }
+    }
+    double dot(const double* a, const double* bb) {
+        k_dot_partial<<<kDotBlocks, ST, 0, s>>>(a, bb, n, partial);
+        k_dot_final<<<1, ST, 0, s>>>(partial, kDotBlocks, scal);
+        cudaMemcpyAsync(h_scal, scal, sizeof(double), cudaMemcpyDeviceToHost, s);
+        const cudaError_t e = cudaStreamSynchronize(s);
+        if (err == cudaSuccess) err = e;
+        return *h_scal;
+    }
+    double norm2(const double* a) { return std::sqrt(dot(a, a)); }
+    void axpy(double a, const double* x, double* y) { k_axpy<<<grid_n(n), ST, 0, s>>>(a, x, y, n); }
+    void copy(double* dst, const double* src) {
+        cudaMemcpyAsync(dst, src, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToDevice, s);
+    }
+    double true_rel(const double* rhs, const double* x, double rhs_norm, double* tmp, double* tmp2) {
+        spmv(b, x, tmp);
+        k_sub<<<grid_n(n), ST, 0, s>>>(rhs, tmp, tmp2, n);
+        return norm2(tmp2) / rhs_norm;
+    }
+    void release() {
+        for (double* p : owned) cudaFreeAsync(p, s);
+        owned.clear();
+    }
+};
+
+// solvers.cpp:54-165
+int gmres(Ctx& c, const double* rhs, double* x, const mcmi_solver_config& cfg, mcmi_solve_report& rep,
+          std::string& msg) {
+    const int64_t n = c.n;
+    const double rhs_norm = c.norm2(rhs);
+    if (rhs_norm == 0.0) {
+        msg = "gmres: rhs is zero";
+        return MCMI_EINVAL;
+    }
+    double* tmp = c.vec();
+    double* tmp2 = c.vec();
+    double* b_prec = c.vec();
+    if (c.prec) c.spmv(c.m, rhs, b_prec);
+    else c.copy(b_prec, rhs);
+    const double b_prec_norm = c.norm2(b_prec);
+    k_fill<<<grid_n(n), ST, 0, c.s>>>(x, 0.0, n);
+    const int64_t restart = cfg.restart;
+    std::vector<double*> v(static_cast<size_t>(restart + 1), nullptr);
+    for (auto& p : v) p = c.vec();
+    double* w = c.vec();
+    if (c.err != cudaSuccess) return MCMI_ENOMEM;
+    std::vector<std::vector<double>> h(restart + 1, std::vector<double>(restart, 0.0));
+    std::vector<double> cs(restart), sn(restart), g(restart + 1);
+    bool done = false;
+    while (!done && rep.iterations < cfg.max_iters) {
+        c.op(x, tmp2, tmp);
+        k_sub<<<grid_n(n), ST, 0, c.s>>>(b_prec, tmp2, w, n);  // r = b_prec - M B x
+        const double beta = c.norm2(w);
+        if (beta < 1e-30) {
+            rep.breakdown = 1;
+            break;
+        }
+        k_div<<<grid_n(n), ST, 0, c.s>>>(w, beta, v[0], n);
+        std::fill(g.begin(), g.end(), 0.0);
+        g[0] = beta;
+        int64_t j = 0;
+        bool cycle_end = false;
+        while (j < restart && !cycle_end) {
+            c.op(v[j], w, tmp);
+            for (int64_t i = 0; i <= j; ++i) {  // modified Gram-Schmidt
+                h[i][j] = c.dot(w, v[i]);
+                c.axpy(-h[i][j], v[i], w);
+            }
+            h[j + 1][j] = c.norm2(w);
+            const bool lucky = h[j + 1][j] < 1e-14;
+            if (!lucky) k_div<<<grid_n(n), ST, 0, c.s>>>(w, h[j + 1][j], v[j + 1], n);
+            for (int64_t i = 0; i < j; ++i) {
+                const double t = cs[i] * h[i][j] + sn[i] * h[i + 1][j];
+                h[i + 1][j] = -sn[i] * h[i][j] + cs[i] * h[i + 1][j];
+                h[i][j] = t;
+            }
+            const double denom = std::sqrt(h[j][j] * h[j][j] + h[j + 1][j] * h[j + 1][j]);
+            if (denom < 1e-30) {
+                cs[j] = 1.0;
+                sn[j] = 0.0;
+            } else {
+                cs[j] = h[j][j] / denom;
+                sn[j] = h[j + 1][j] / denom;
+            }
+            h[j][j] = cs[j] * h[j][j] + sn[j] * h[j + 1][j];
+            h[j + 1][j] = 0.0;
+            g[j + 1] = -sn[j] * g[j];
+            g[j] = cs[j] * g[j];
+            ++j;
+            ++rep.iterations;
+            const double rel = std::abs(g[j]) / b_prec_norm;
+            if (rel <= cfg.rel_tol || lucky || rep.iterations >= cfg.max_iters) {
+                cycle_end = true;
+                if (lucky && rel > cfg.rel_tol) rep.breakdown = 1;
+            }
+        }
+        std::vector<double> y(static_cast<size_t>(j), 0.0);
+        for (int64_t i = j; i-- > 0;) {
+            double sacc = g[i];
+            for (int64_t k = i + 1; k < j; ++k) sacc -= h[i][k] * y[k];
+            y[i] = h[i][i] != 0.0 ? sacc / h[i][i] : 0.0;
+        }
+        for (int64_t k = 0; k < j; ++k) c.axpy(y[k], v[k], x);
+        const double true_rel = c.true_rel(rhs, x, rhs_norm, tmp, tmp2);
+        if (true_rel <= cfg.rel_tol) {
+            rep.converged = 1;
+            done = true;
+        } else if (rep.breakdown) {
+            done = true;
+        }
+    }
+    rep.final_rel_residual = c.true_rel(rhs, x, rhs_norm, tmp, tmp2);
+    rep.converged = rep.final_rel_residual <= cfg.rel_tol;
+    return c.err == cudaSuccess ? MCMI_OK : MCMI_ECUDA;
+}
+
+// solvers.cpp:167-238
+int bicgstab(Ctx& c, const double* rhs, double* x, const mcmi_solver_config& cfg, mcmi_solve_report& rep,
+             std::string& msg) {
+    const int64_t n = c.n;
+    const double rhs_norm = c.norm2(rhs);
+    if (rhs_norm == 0.0) {
+        msg = "bicgstab: rhs is zero";
+        return MCMI_EINVAL;
+    }
+    double* tmp = c.vec();
+    double* tmp2 = c.vec();
+    double* b_prec = c.vec();
+    double* r = c.vec();
+    double* r0 = c.vec();
+    double* p = c.vec();
+    double* vv = c.vec();
+    double* s = c.vec();
+    double* t = c.vec();
+    if (c.err != cudaSuccess) return MCMI_ENOMEM;
+    if (c.prec) c.spmv(c.m, rhs, b_prec);
+    else c.copy(b_prec, rhs);
+    const double b_prec_norm = c.norm2(b_prec);
+    k_fill<<<grid_n(n), ST, 0, c.s>>>(x, 0.0, n);
+    c.copy(r, b_prec);
+    c.copy(r0, r);
+    k_fill<<<grid_n(n), ST, 0, c.s>>>(p, 0.0, n);
+    k_fill<<<grid_n(n), ST, 0, c.s>>>(vv, 0.0, n);
+    double rho = 1.0, alpha = 1.0, omega = 1.0;
+    while (rep.iterations < cfg.max_iters) {
+        const double rho1 = c.dot(r0, r);
+        if (std::abs(rho1) < 1e-30) {
+            rep.breakdown = 1;
+            break;
+        }
+        const double beta = (rho1 / rho) * (alpha / omega);
+        k_bicg_p<<<grid_n(n), ST, 0, c.s>>>(r, beta, omega, vv, p, n);
+        c.op(p, vv, tmp);
+        const double r0v = c.dot(r0, vv);
+        if (std::abs(r0v) < 1e-30) {
+            rep.breakdown = 1;
+            break;
+        }
+        alpha = rho1 / r0v;
+        c.copy(s, r);
+        c.axpy(-alpha, vv, s);
+        c.op(s, t, tmp);
+        const double tt = c.dot(t, t);
+        omega = tt > 0.0 ? c.dot(t, s) / tt : 0.0;
+        c.axpy(alpha, p, x);
+        c.axpy(omega, s, x);
+        c.copy(r, s);
+        c.axpy(-omega, t, r);
+        rho = rho1;
+        ++rep.iterations;
+        const double rel = c.norm2(r) / b_prec_norm;
+        if (rel <= cfg.rel_tol && c.true_rel(rhs, x, rhs_norm, tmp, tmp2) <= cfg.rel_tol) break;
+        if (omega == 0.0) {
+            rep.breakdown = 1;
+            break;
+        }
+    }
+    rep.final_rel_residual = c.true_rel(rhs, x, rhs_norm, tmp, tmp2);
+    rep.converged = rep.final_rel_residual <= cfg.rel_tol;
+    return c.err == cudaSuccess ? MCMI_OK : MCMI_ECUDA;
+}
+
+}  // namespace
+
+int solve_device(const mcmi_csr_view& b, const mcmi_csr_view* m, const double* rhs_in, double* x,
+                 const mcmi_solver_config& cfg, cudaStream_t s, mcmi_solve_report* rep, std::string& msg) {
+    std::memset(rep, 0, sizeof(*rep));
+    if (m && m->n != b.n) {
+        msg = "solver: preconditioner dimension mismatch";
+        return MCMI_EINVAL;
+    }
+    if (cfg.method == 0 && cfg.restart < 1) {
+        msg = "gmres: restart must be positive";
+        return MCMI_EINVAL;
+    }
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, s);
+    Ctx c;
+    c.s = s;
+    c.n = b.n;
+    c.b = DevCsr{b.n, b.row_ptr, b.col_idx, b.values};
+    c.prec = m != nullptr;
+    if (m) c.m = DevCsr{m->n, m->row_ptr, m->col_idx, m->values};
+    cudaMallocAsync(&c.partial, kDotBlocks * sizeof(double), s);
+    cudaMallocAsync(&c.scal, sizeof(double), s);
+    cudaMallocHost(&c.h_scal, sizeof(double));
+    const double* rhs = rhs_in;
+    double* ones_rhs = nullptr;
+    if (!rhs) {  // ones_product_rhs (solvers.cpp:46-48): rhs = B * 1
+        double* ones = c.vec();
+        ones_rhs = c.vec();
+        k_fill<<<grid_n(b.n), ST, 0, s>>>(ones, 1.0, b.n);
+        c.spmv(c.b, ones, ones_rhs);
+        rhs = ones_rhs;
+    }
+    const int code = cfg.method == 0 ? gmres(c, rhs, x, cfg, *rep, msg) : bicgstab(c, rhs, x, cfg, *rep, msg);
+    c.release();
+    cudaFreeAsync(c.partial, s);
+    cudaFreeAsync(c.scal, s);
+    cudaEventRecord(e1, s);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    rep->ms = ms;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFreeHost(c.h_scal);
+    if (code == MCMI_ECUDA) msg = std::string("solver: ") + cudaGetErrorString(cudaGetLastError());
+    return code;
+}
+
+}  // namespace mcmi
+
+extern "C" {
+
+void mcmi_solver_config_default(mcmi_solver_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->method = MCMI_SOLVER_GMRES;
+    c->rel_tol = 1e-6;
+    c->max_iters = 30000;
+    c->restart = 50;
+}
+
+int mcmi_solve_device(const mcmi_csr_view* b, const mcmi_csr_view* m, const double* rhs, double* x,
+                      const mcmi_solver_config* cfg, int device, void* stream, mcmi_solve_report* rep,
+                      char* err, size_t errlen) {
+    std::string msg;
+    int code = MCMI_OK;
+    if (!b || !x || !cfg || !rep) {
+        code = MCMI_EINVAL;
+        msg = "null argument";
+    } else if (cudaSetDevice(device) != cudaSuccess) {
+        code = MCMI_ENODEV;
+        msg = "cudaSetDevice failed";
+    } else {
+        code = mcmi::solve_device(*b, m, rhs, x, *cfg, static_cast<cudaStream_t>(stream), rep, msg);
+    }
+    if (err && errlen) {
+        std::strncpy(err, msg.c_str(), errlen - 1);
+        err[errlen - 1] = 0;
+    }
+    return code;
+}
+
+}  // extern "C"
