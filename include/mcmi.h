@@ -119,6 +119,17 @@ int mcmi_build(const mcmi_csr_view* b, const mcmi_config* cfg, mcmi_result** out
  * transition tables always cover all n states. */
 int mcmi_build_rows(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_begin,
                     int64_t row_end, mcmi_result** out, char* err, size_t errlen);
+/* Streamed variant: builds rows [row_begin, row_end) straight into caller-owned
+ * host arrays (pinned memory gives full PCIe bandwidth), overlapping the
+ * device->host copy of each row chunk with the walks of the next.  row_ptr
+ * [rows+1]; col_idx / values hold `capacity` entries; chains_used /
+ * entries_before [rows] may be NULL.  *nnz receives the entry count; if it
+ * exceeds capacity the call returns MCMI_ENOMEM (and *nnz says how much is
+ * needed).  Same results as mcmi_build_rows. */
+int mcmi_build_into(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_begin, int64_t row_end,
+                    int64_t* row_ptr, int64_t* col_idx, double* values, int64_t capacity,
+                    int64_t* chains_used, int64_t* entries_before, int64_t* nnz, mcmi_stats* stats,
+                    char* err, size_t errlen);
 int mcmi_result_sizes(const mcmi_result* r, int64_t* n, int64_t* nnz);
 /* Any pointer may be NULL.  row_ptr[n+1], col_idx[nnz], values[nnz],
  * chains_used[n] / entries_before[n] = RowMeta (mc_engine.hpp:33-36),
@@ -189,6 +200,12 @@ int mcmi_solve_device(const mcmi_csr_view* b_dev, const mcmi_csr_view* m_dev, co
 /* cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, stream): copies an
  * engine output into caller-owned host or device memory. */
 int mcmi_copy(void* dst, const void* src, size_t bytes, void* stream);
+
+/* Page-locks caller memory for this library's DMA (cudaHostRegister): host
+ * buffers reused across mcmi_build_into calls should be registered once so
+ * the device->host copies run asynchronously at full PCIe bandwidth. */
+int mcmi_host_register(void* ptr, size_t bytes);
+int mcmi_host_unregister(void* ptr);
 
 /* Library identification: returns "mcmi <abi> sm_100a". */
 const char* mcmi_version(void);

@@ -17,9 +17,10 @@ MCMI_OK, MCMI_EINVAL, MCMI_ESPLIT, MCMI_ERANGE, MCMI_ECUDA, MCMI_ENOMEM, MCMI_EN
 
 #: every symbol include/mcmi.h declares
 EXPORTS = [
-    "mcmi_config_default", "mcmi_build", "mcmi_build_rows", "mcmi_result_sizes", "mcmi_result_copy",
+    "mcmi_config_default", "mcmi_build", "mcmi_build_rows", "mcmi_build_into", "mcmi_result_sizes", "mcmi_result_copy",
     "mcmi_result_stats", "mcmi_result_free", "mcmi_engine_create", "mcmi_engine_destroy",
     "mcmi_engine_build", "mcmi_copy", "mcmi_version", "mcmi_solver_config_default", "mcmi_solve_device",
+    "mcmi_host_register", "mcmi_host_unregister",
 ]
 
 
@@ -111,6 +112,9 @@ def load(path: str | None = None):
                              C.c_char_p, C.c_size_t]
     L.mcmi_build_rows.argtypes = [C.POINTER(mcmi_csr_view), C.POINTER(mcmi_config), C.c_int64, C.c_int64,
                                   C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+    L.mcmi_build_into.argtypes = [C.POINTER(mcmi_csr_view), C.POINTER(mcmi_config), C.c_int64, C.c_int64,
+                                  C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
+                                  C.POINTER(C.c_int64), C.POINTER(mcmi_stats), C.c_char_p, C.c_size_t]
     L.mcmi_result_sizes.argtypes = [C.c_void_p, _i64p, _i64p]
     L.mcmi_result_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    _i64p, _i64p]
@@ -125,6 +129,8 @@ def load(path: str | None = None):
                                     C.c_char_p, C.c_size_t]
     L.mcmi_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]
     L.mcmi_version.restype = C.c_char_p
+    L.mcmi_host_register.argtypes = [C.c_void_p, C.c_size_t]
+    L.mcmi_host_unregister.argtypes = [C.c_void_p]
     L.mcmi_solver_config_default.argtypes = [C.POINTER(mcmi_solver_config)]
     L.mcmi_solver_config_default.restype = None
     L.mcmi_solve_device.argtypes = [C.POINTER(mcmi_csr_view), C.POINTER(mcmi_csr_view), C.c_void_p, C.c_void_p,

@@ -126,7 +126,20 @@ __global__ void k_compact(const int* __restrict__ stage_col, const double* __res
     }
 }
 
+__global__ void k_add_offset(int64_t* __restrict__ a, int64_t add, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        a[i] += add;
+}
+
 }  // namespace
+
+cudaError_t launch_add_offset(int64_t* a, int64_t add, int64_t n, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    int64_t blocks = (n + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    k_add_offset<<<(unsigned)blocks, 256, 0, s>>>(a, add, n);
+    return cudaGetLastError();
+}
 
 size_t scan_scratch_bytes(int64_t n) {
     const int64_t nb = (n + SCAN_TILE - 1) / SCAN_TILE;

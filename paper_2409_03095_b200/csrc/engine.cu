@@ -155,6 +155,21 @@ struct mcmi_engine {
     DevBuf ovf[2];
     DevBuf gscratch;  // global accumulator tier
     DevBuf out_rp, out_col, out_val;
+    // streamed build (mcmi_build_into): double-buffered output slabs + copy stream
+    DevBuf rp_slab[2], col_slab[2], val_slab[2];
+    cudaStream_t copy = nullptr;
+    cudaEvent_t copy_done[2] = {};
+    cudaEvent_t chunk_ready = nullptr;
+    cudaError_t ensure_copy_stream() {
+        if (copy) return cudaSuccess;
+        cudaError_t r = cudaStreamCreateWithFlags(&copy, cudaStreamNonBlocking);
+        for (auto& ev : copy_done)
+            if (r == cudaSuccess) r = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+        if (r == cudaSuccess) r = cudaEventCreateWithFlags(&chunk_ready, cudaEventDisableTiming);
+        if (r == cudaSuccess)  // both slabs start released
+            for (auto& ev : copy_done) cudaEventRecord(ev, copy);
+        return r;
+    }
     Reductions* h_red = nullptr;          // pinned
     unsigned long long* h_ctr = nullptr;  // pinned [8]
     int64_t* h_i64 = nullptr;             // pinned [4]
@@ -208,8 +223,13 @@ void engine_release(mcmi_engine* e) {
                       &e->colA, &e->b1, &e->scan_tmp, &e->cq_tmp, &e->stage_col, &e->stage_val,
                       &e->row_cnt, &e->row_src, &e->chains_used, &e->entries_before,
                       &e->counters, &e->ovf[0], &e->ovf[1], &e->gscratch, &e->out_rp, &e->out_col,
-                      &e->out_val})
+                      &e->out_val, &e->rp_slab[0], &e->rp_slab[1], &e->col_slab[0], &e->col_slab[1],
+                      &e->val_slab[0], &e->val_slab[1]})
         b->release();
+    for (auto& ev : e->copy_done)
+        if (ev) cudaEventDestroy(ev);
+    if (e->chunk_ready) cudaEventDestroy(e->chunk_ready);
+    if (e->copy) cudaStreamDestroy(e->copy);
     for (auto& ev : e->ev)
         if (ev) cudaEventDestroy(ev);
     if (e->own) cudaStreamDestroy(e->own);
@@ -256,9 +276,19 @@ Tier make_global_tier(int64_t bound, int64_t max_len) {
 }
 
 // The full build of rows [row_begin, row_end) from device CSR `b`.
+// Caller-owned host arrays for the streamed build (mcmi_build_into).
+struct HostSink {
+    int64_t* row_ptr;
+    int64_t* col_idx;
+    double* values;
+    int64_t capacity;
+    int64_t* chains_used;
+    int64_t* entries_before;
+};
+
 Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& cfg,
                     int64_t row_begin, int64_t row_end, cudaStream_t s, mcmi_device_csr* out,
-                    mcmi_stats* stats) {
+                    mcmi_stats* stats, const HostSink* sink = nullptr) {
     const int64_t n = b.n;
     mcmi_stats st{};
     if (n < 0) return fail(MCMI_EINVAL, "negative dimension");
@@ -489,12 +519,11 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
 
     // Pilot: when rows may overflow the first tier, build the first rows on the
     // last tier (which cannot overflow: its cap_limit >= bound), and start the
-    // rest on the smallest tier that held every pilot row.  Rows the pilot
-    // under-estimates still overflow into the next tiers, so results never
-    // depend on this choice.
+    // rest on the tier a cost model picks from the pilot rows' distinct-column
+    // counts.  Rows the pilot under-estimates still overflow into the next
+    // tiers, so results never depend on this choice.
     size_t t0 = 0;
-    int64_t offset = 0;
-    int64_t work = rows;
+    int64_t pilot_rows = 0;
     const int64_t pilot = std::min<int64_t>(1024, rows / 4);
     if (tiers.size() > 1 && pilot >= 64) {
         int64_t ovf = 0;
@@ -506,11 +535,10 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
                                  cudaMemcpyDeviceToHost, s),
                  "read pilot");
         MCMI_TRY(cudaStreamSynchronize(s), "read pilot");
-        // Start tier by a cost model over the pilot rows: a row of s distinct
-        // columns costs c_t on the tier that holds it and ~c_t * limit_t / s on
-        // each tier it overflows first (it aborts once the table is full).
-        // Relative costs c_t follow occupancy: smem <= 256: 1, smem 1024: 2,
-        // global: 3 (measured on the C5 grid, tools/c5_sweep.py).
+        // A row of s distinct columns costs c_t on the tier that holds it and
+        // ~c_t * limit_t / s on each tier it overflows first (it aborts once the
+        // table is full).  Relative costs follow occupancy: smem <= 256: 1,
+        // smem 1024: 2, global: 3 (measured on the C5 grid, tools/c5_sweep.py).
         auto tier_cost = [](const Tier& t) { return t.global ? 3.0 : (t.cap <= 256 ? 1.0 : 2.0); };
         double best = 0.0;
         for (size_t c0 = 0; c0 < tiers.size(); ++c0) {
@@ -531,41 +559,149 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
             }
         }
         st.hash_cap = tiers[t0].cap;
-        offset = pilot;
-        work = rows - pilot;
+        pilot_rows = pilot;
     }
-    const int* row_list = nullptr;
-    for (size_t ti = t0; ti < tiers.size() && work > 0; ++ti) {
-        int64_t overflowed = 0;
-        Status ts = run_tier(tiers[ti], work, row_list, row_list ? 0 : offset, &overflowed);
-        if (ts.code) return ts;
-        if (ti > t0) st.rows_retried += work;
-        work = overflowed;
-        row_list = e->ovf[cur].as<int>();
-        cur ^= 1;
+    // Walks rows [lo, hi) (local) starting on tier t0, retrying overflows.
+    auto walk_rows = [&](int64_t lo, int64_t hi) -> Status {
+        int64_t work = hi - lo;
+        const int* row_list = nullptr;
+        for (size_t ti = t0; ti < tiers.size() && work > 0; ++ti) {
+            int64_t overflowed = 0;
+            Status ts = run_tier(tiers[ti], work, row_list, row_list ? 0 : lo, &overflowed);
+            if (ts.code) return ts;
+            if (ti > t0) st.rows_retried += work;
+            work = overflowed;
+            row_list = e->ovf[cur].as<int>();
+            cur ^= 1;
+        }
+        if (work > 0)
+            return fail(MCMI_ENOMEM, std::to_string(work) + " rows overflowed every accumulator tier");
+        return ok();
+    };
+
+    int64_t out_nnz = 0;
+    if (!sink) {
+        // ---- one pass: all rows, then assembly into the engine's buffers
+        Status ws = walk_rows(pilot_rows, rows);
+        if (ws.code) return ws;
+        MCMI_TRY(cudaEventRecord(e->ev[2], s), "cudaEventRecord");
+        // ---- assembly (mc_engine.cpp:207-225)
+        MCMI_TRY(e->out_rp.ensure((rows + 1) * sizeof(int64_t)), "alloc row_ptr");
+        MCMI_TRY(scan_rows_exclusive(e->row_cnt.as<int>(), e->out_rp.as<int64_t>(), rows, e->scan_tmp.p, s),
+                 "scan rows");
+        MCMI_TRY(cudaMemcpyAsync(e->h_i64, e->out_rp.as<int64_t>() + rows, sizeof(int64_t),
+                                 cudaMemcpyDeviceToHost, s),
+                 "read nnz");
+        MCMI_TRY(cudaStreamSynchronize(s), "scan rows");
+        out_nnz = e->h_i64[0];
+        MCMI_TRY(e->out_col.ensure(std::max<int64_t>(out_nnz, 1) * sizeof(int64_t)), "alloc col");
+        MCMI_TRY(e->out_val.ensure(std::max<int64_t>(out_nnz, 1) * sizeof(double)), "alloc val");
+        MCMI_TRY(launch_compact(e->stage_col.as<int>(), e->stage_val.as<double>(), e->row_src.as<int64_t>(),
+                                e->row_cnt.as<int>(), e->out_rp.as<int64_t>(), rows, e->out_col.as<int64_t>(),
+                                e->out_val.as<double>(), s),
+                 "compact");
+        st.launches += (rows > 0 ? 3 : 1) + (rows > 0 ? 1 : 0);
+    } else {
+        // ---- streamed: row chunks; chunk c's device->host copy (copy stream)
+        // overlaps chunk c+1's walk (compute stream).  Double-buffered slabs.
+        const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(16, (rows + 131071) / 131072));
+        const int64_t chunk = (rows + nchunk - 1) / nchunk;
+        MCMI_TRY(e->ensure_copy_stream(), "copy stream");
+        MCMI_TRY(cudaStreamSynchronize(e->copy), "drain copies");
+        // row pointers of all chunks accumulate in out_rp; only col/val stream per chunk
+        // (small per-chunk copies into pageable memory would block the host behind
+        // the copy stream and serialise it with the walks)
+        MCMI_TRY(e->out_rp.ensure((rows + 1) * sizeof(int64_t)), "alloc row_ptr");
+        int64_t slab_cap = static_cast<int64_t>(std::min(e->col_slab[0].cap / sizeof(int64_t),
+                                                         e->val_slab[0].cap / sizeof(double)));
+        int64_t running = 0;
+        bool fits = true;
+        // MCMI_STREAM_DEBUG=1: per-chunk device timestamps of walk and copy
+        const bool dbg = getenv("MCMI_STREAM_DEBUG") != nullptr;
+        std::vector<cudaEvent_t> dev(dbg ? 4 * nchunk : 0);
+        for (auto& ev : dev) cudaEventCreate(&ev);
+        for (int64_t c = 0; c < nchunk; ++c) {
+            if (dbg) cudaEventRecord(dev[4 * c], s);
+            const int64_t lo = c * chunk, hi = std::min(rows, lo + chunk);
+            if (lo >= hi) break;
+            if (c > 0) pool_used = 0;  // staging reused per chunk (chunk 0 keeps the pilot rows' slots)
+            Status ws = walk_rows(c == 0 ? pilot_rows : lo, hi);
+            if (ws.code) return ws;
+            if (dbg) cudaEventRecord(dev[4 * c + 1], s);
+            const int64_t cr = hi - lo;
+            int64_t* rp_slab = e->out_rp.as<int64_t>() + lo;  // chunk-local offsets, then global
+            // wait until chunk c-2's copies released this slab pair
+            MCMI_TRY(cudaStreamWaitEvent(s, e->copy_done[c & 1], 0), "wait copy");
+            MCMI_TRY(scan_rows_exclusive(e->row_cnt.as<int>() + lo, rp_slab, cr, e->scan_tmp.p, s), "scan rows");
+            MCMI_TRY(cudaMemcpyAsync(e->h_i64, rp_slab + cr, sizeof(int64_t), cudaMemcpyDeviceToHost, s),
+                     "read chunk nnz");
+            MCMI_TRY(cudaStreamSynchronize(s), "scan rows");
+            const int64_t cn = e->h_i64[0];
+            if (running + cn > sink->capacity) fits = false;
+            if (fits) {
+                if (cn > slab_cap) {
+                    MCMI_TRY(cudaStreamSynchronize(e->copy), "drain copies");
+                    for (int q = 0; q < 2; ++q) {
+                        MCMI_TRY(e->col_slab[q].ensure(std::max<int64_t>(cn, 1) * sizeof(int64_t)), "alloc slab");
+                        MCMI_TRY(e->val_slab[q].ensure(std::max<int64_t>(cn, 1) * sizeof(double)), "alloc slab");
+                    }
+                    slab_cap = cn;
+                }
+                int64_t* cs = e->col_slab[c & 1].as<int64_t>();
+                double* vs = e->val_slab[c & 1].as<double>();
+                MCMI_TRY(launch_compact(e->stage_col.as<int>(), e->stage_val.as<double>(),
+                                        e->row_src.as<int64_t>() + lo, e->row_cnt.as<int>() + lo, rp_slab, cr, cs,
+                                        vs, s),
+                         "compact");
+                MCMI_TRY(launch_add_offset(rp_slab, running, cr, s), "row_ptr offset");
+                MCMI_TRY(cudaEventRecord(e->chunk_ready, s), "cudaEventRecord");
+                MCMI_TRY(cudaStreamWaitEvent(e->copy, e->chunk_ready, 0), "wait chunk");
+                if (dbg) cudaEventRecord(dev[4 * c + 2], e->copy);
+                auto d2h = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+                    return bytes ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, e->copy) : cudaSuccess;
+                };
+                MCMI_TRY(d2h(sink->col_idx + running, cs, cn * sizeof(int64_t)), "D2H col");
+                MCMI_TRY(d2h(sink->values + running, vs, cn * sizeof(double)), "D2H val");
+                MCMI_TRY(cudaEventRecord(e->copy_done[c & 1], e->copy), "cudaEventRecord");
+                if (dbg) cudaEventRecord(dev[4 * c + 3], e->copy);
+                st.launches += 5;
+            }
+            running += cn;
+        }
+        MCMI_TRY(cudaEventRecord(e->ev[2], s), "cudaEventRecord");
+        MCMI_TRY(cudaStreamSynchronize(e->copy), "D2H");
+        if (dbg) {
+            for (int64_t c = 0; c < nchunk; ++c) {
+                float w0 = 0, w1 = 0, c0 = 0, c1 = 0;
+                cudaEventElapsedTime(&w0, e->ev[0], dev[4 * c]);
+                cudaEventElapsedTime(&w1, e->ev[0], dev[4 * c + 1]);
+                cudaEventElapsedTime(&c0, e->ev[0], dev[4 * c + 2]);
+                cudaEventElapsedTime(&c1, e->ev[0], dev[4 * c + 3]);
+                fprintf(stderr, "chunk %lld walk %.2f-%.2f copy %.2f-%.2f ms\n", static_cast<long long>(c), w0, w1,
+                        c0, c1);
+            }
+            for (auto& ev : dev) cudaEventDestroy(ev);
+        }
+        out_nnz = running;
+        if (fits) {  // row pointers and RowMeta: one copy each, after the walks
+            auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
+                return (dst && bytes) ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s) : cudaSuccess;
+            };
+            MCMI_TRY(cp(sink->row_ptr, e->out_rp.p, rows * sizeof(int64_t)), "D2H row_ptr");
+            MCMI_TRY(cp(sink->chains_used, e->chains_used.p, rows * sizeof(int64_t)), "D2H meta");
+            MCMI_TRY(cp(sink->entries_before, e->entries_before.p, rows * sizeof(int64_t)), "D2H meta");
+            MCMI_TRY(cudaStreamSynchronize(s), "D2H row_ptr");
+            sink->row_ptr[rows] = running;
+        }
+        if (!fits) {
+            st.nnz = out_nnz;
+            if (stats) *stats = st;
+            return fail(MCMI_ENOMEM, "output capacity " + std::to_string(sink->capacity) + " < nnz " +
+                                         std::to_string(out_nnz));
+        }
     }
-    if (work > 0)
-        return fail(MCMI_ENOMEM, std::to_string(work) + " rows overflowed every accumulator tier");
     st.walk_steps = static_cast<int64_t>(total_steps);
     st.walk_deg_sum = static_cast<int64_t>(total_deg);
-    MCMI_TRY(cudaEventRecord(e->ev[2], s), "cudaEventRecord");
-
-    // ---- assembly (mc_engine.cpp:207-225)
-    MCMI_TRY(e->out_rp.ensure((rows + 1) * sizeof(int64_t)), "alloc row_ptr");
-    MCMI_TRY(scan_rows_exclusive(e->row_cnt.as<int>(), e->out_rp.as<int64_t>(), rows, e->scan_tmp.p, s),
-             "scan rows");
-    MCMI_TRY(cudaMemcpyAsync(e->h_i64, e->out_rp.as<int64_t>() + rows, sizeof(int64_t),
-                             cudaMemcpyDeviceToHost, s),
-             "read nnz");
-    MCMI_TRY(cudaStreamSynchronize(s), "scan rows");
-    const int64_t out_nnz = e->h_i64[0];
-    MCMI_TRY(e->out_col.ensure(std::max<int64_t>(out_nnz, 1) * sizeof(int64_t)), "alloc col");
-    MCMI_TRY(e->out_val.ensure(std::max<int64_t>(out_nnz, 1) * sizeof(double)), "alloc val");
-    MCMI_TRY(launch_compact(e->stage_col.as<int>(), e->stage_val.as<double>(), e->row_src.as<int64_t>(),
-                            e->row_cnt.as<int>(), e->out_rp.as<int64_t>(), rows, e->out_col.as<int64_t>(),
-                            e->out_val.as<double>(), s),
-             "compact");
-    st.launches += (rows > 0 ? 3 : 1) + (rows > 0 ? 1 : 0);
     MCMI_TRY(cudaEventRecord(e->ev[3], s), "cudaEventRecord");
     MCMI_TRY(cudaStreamSynchronize(s), "assembly");
     float t01 = 0, t12 = 0, t23 = 0, t03 = 0;
@@ -737,6 +873,47 @@ int mcmi_build_rows(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_
     return report(st, err, errlen);
 }
 
+int mcmi_build_into(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_begin, int64_t row_end,
+                    int64_t* row_ptr, int64_t* col_idx, double* values, int64_t capacity,
+                    int64_t* chains_used, int64_t* entries_before, int64_t* nnz, mcmi_stats* stats,
+                    char* err, size_t errlen) {
+    if (!b || !cfg || !row_ptr || !nnz || (capacity > 0 && (!col_idx || !values)))
+        return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    Status st;
+    mcmi_engine* e = acquire_engine(cfg->device, &st);
+    if (!e) return report(st, err, errlen);
+    auto run = [&]() -> Status {
+        const int64_t n = b->n;
+        if (n < 0) return fail(MCMI_EINVAL, "negative dimension");
+        const int64_t bnnz = n > 0 ? b->row_ptr[n] : 0;
+        cudaStream_t s = e->own;
+        void *d_rp = nullptr, *d_ci = nullptr, *d_v = nullptr;
+        MCMI_TRY(cudaMallocAsync(&d_rp, (std::max<int64_t>(n, 0) + 1) * sizeof(int64_t), s), "alloc B");
+        MCMI_TRY(cudaMallocAsync(&d_ci, std::max<int64_t>(bnnz, 1) * sizeof(int64_t), s), "alloc B");
+        MCMI_TRY(cudaMallocAsync(&d_v, std::max<int64_t>(bnnz, 1) * sizeof(double), s), "alloc B");
+        MCMI_TRY(cudaMemcpyAsync(d_rp, b->row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDefault, s), "H2D");
+        if (bnnz > 0) {
+            MCMI_TRY(cudaMemcpyAsync(d_ci, b->col_idx, bnnz * sizeof(int64_t), cudaMemcpyDefault, s), "H2D");
+            MCMI_TRY(cudaMemcpyAsync(d_v, b->values, bnnz * sizeof(double), cudaMemcpyDefault, s), "H2D");
+        }
+        const mcmi_csr_view dv{n, static_cast<int64_t*>(d_rp), static_cast<int64_t*>(d_ci),
+                               static_cast<double*>(d_v)};
+        HostSink sink{row_ptr, col_idx, values, capacity, chains_used, entries_before};
+        mcmi_device_csr dc{};
+        mcmi_stats ls{};
+        Status bst = engine_build(e, dv, *cfg, row_begin, row_end, s, &dc, &ls, &sink);
+        cudaFreeAsync(d_rp, s);
+        cudaFreeAsync(d_ci, s);
+        cudaFreeAsync(d_v, s);
+        *nnz = ls.nnz;
+        if (stats) *stats = ls;
+        return bst;
+    };
+    st = run();
+    release_engine(e);
+    return report(st, err, errlen);
+}
+
 int mcmi_result_sizes(const mcmi_result* r, int64_t* n, int64_t* nnz) {
     if (!r) return MCMI_EINVAL;
     if (n) *n = r->n;
@@ -775,6 +952,23 @@ void mcmi_result_free(mcmi_result* r) {
     if (!r) return;
     if (r->engine) release_engine(r->engine);
     delete r;
+}
+
+int mcmi_host_register(void* ptr, size_t bytes) {
+    if (!ptr || !bytes) return MCMI_OK;
+    const cudaError_t e = cudaHostRegister(ptr, bytes, cudaHostRegisterDefault);
+    if (e == cudaErrorHostMemoryAlreadyRegistered) {
+        cudaGetLastError();
+        return MCMI_OK;
+    }
+    return e == cudaSuccess ? MCMI_OK : MCMI_ECUDA;
+}
+
+int mcmi_host_unregister(void* ptr) {
+    if (!ptr) return MCMI_OK;
+    const cudaError_t e = cudaHostUnregister(ptr);
+    if (e != cudaSuccess) cudaGetLastError();
+    return e == cudaSuccess ? MCMI_OK : MCMI_ECUDA;
 }
 
 int mcmi_copy(void* dst, const void* src, size_t bytes, void* stream) {

@@ -118,6 +118,7 @@ cudaError_t scan_u32_exclusive(const unsigned* in, unsigned* out, int64_t n, voi
                                cudaStream_t s);  // out[n] = total
 cudaError_t scan_rows_exclusive(const int* in, int64_t* out, int64_t n, void* scratch,
                                 cudaStream_t s);  // out[n] = total
+cudaError_t launch_add_offset(int64_t* a, int64_t add, int64_t n, cudaStream_t s);
 cudaError_t launch_compact(const int* stage_col, const double* stage_val, const int64_t* row_src,
                            const int* row_cnt, const int64_t* row_ptr, int64_t rows,
                            int64_t* col_out, double* val_out, cudaStream_t s);

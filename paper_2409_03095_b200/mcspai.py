@@ -228,6 +228,23 @@ def compute_preconditioner(b: CsrMatrix, cfg: McConfig | None = None, n_threads:
     h = C.c_void_p()
     err = C.create_string_buffer(1024)
     lo, hi = rows if rows is not None else (0, -1)
+    if out is not None and out.get("values") is not None:
+        # streamed build into the caller's (pinned) arrays: the device->host copy
+        # of each row chunk overlaps the walks of the next (mcmi_build_into)
+        nrows = (b.n if hi < 0 else hi) - lo
+        cap = int(min(out["col_idx"].size, out["values"].size))
+        rp, ci, v = out["row_ptr"][: nrows + 1], out["col_idx"], out["values"]
+        cu, eb = np.empty(max(nrows, 1), np.int64), np.empty(max(nrows, 1), np.int64)
+        nnz = C.c_int64()
+        st = L.mcmi_stats()
+        code = lib.mcmi_build_into(C.byref(view), C.byref(c), lo, hi, rp.ctypes.data, ci.ctypes.data,
+                                   v.ctypes.data, cap, cu.ctypes.data, eb.ctypes.data, C.byref(nnz),
+                                   C.byref(st), err, 1024)
+        if not (code == L.MCMI_ENOMEM and nnz.value > cap):  # too small: fall back to the handle path
+            raise_for(code, err.value.decode(errors="replace"))
+            k = nnz.value
+            return ApproxInverse(CsrMatrix(nrows, rp, ci[:k], v[:k]), RowMeta(cu[:nrows], eb[:nrows]), cfg,
+                                 ChainBudget(st.n_chains, st.max_len), int(cfg.master_seed), st.as_dict())
     code = lib.mcmi_build_rows(C.byref(view), C.byref(c), lo, hi, C.byref(h), err, 1024)
     raise_for(code, err.value.decode(errors="replace"))
     try:
@@ -250,6 +267,22 @@ def compute_preconditioner(b: CsrMatrix, cfg: McConfig | None = None, n_threads:
         lib.mcmi_result_free(h)
     return ApproxInverse(CsrMatrix(n, rp, ci, v), RowMeta(cu, eb), cfg, ChainBudget(nc.value, ml.value),
                          int(cfg.master_seed), st.as_dict())
+
+
+def host_register(*arrays):
+    """Page-locks numpy arrays for the library's DMA (mcmi_host_register) so
+    streamed builds into them overlap the device->host copy with the walks."""
+    lib = L.load()
+    for a in arrays:
+        if a is not None and a.size:
+            raise_for(lib.mcmi_host_register(a.ctypes.data, a.nbytes), "cudaHostRegister failed")
+
+
+def host_unregister(*arrays):
+    lib = L.load()
+    for a in arrays:
+        if a is not None and a.size:
+            lib.mcmi_host_unregister(a.ctypes.data)
 
 
 def compute_preconditioner_serial(b: CsrMatrix, cfg: McConfig | None = None) -> ApproxInverse:

@@ -336,3 +336,28 @@ def test_invalid_row_ptr_rejected_without_fault(mc):
     # the device is still healthy afterwards
     ok = mc.compute_preconditioner(mc.CsrMatrix.identity(4), mc.McConfig(alpha=1.0))
     assert ok.m.nnz() == 4
+
+
+@pytest.mark.parametrize("rng", [0, 1])
+def test_streamed_build_into_equals_handle_path(mc, rng):
+    # mcmi_build_into (row chunks, D2H overlapped) == mcmi_build_rows, incl. a
+    # multi-chunk build and a too-small buffer (falls back to the handle path)
+    from paper_2409_03095_b200 import generators as G
+    for b, cfg in ((_csr(mc, "brusselator:32"), mc.McConfig(epsilon=.05, delta=.01, alpha=1.5, retain_k=32,
+                                                             master_seed=20260826, rng_mode=rng)),
+                   (G.laplacian3d(64), mc.McConfig(rng_mode=rng))):
+        want = mc.compute_preconditioner(b, cfg)
+        for cap in (want.m.nnz() + 7, 10):
+            out = {"row_ptr": np.empty(b.n + 1, np.int64), "col_idx": np.empty(cap, np.int64),
+                   "values": np.empty(cap)}
+            got = mc.compute_preconditioner(b, cfg, out=out)
+            assert got.m == want.m
+            assert np.array_equal(got.row_meta.chains_used, want.row_meta.chains_used)
+            assert np.array_equal(got.row_meta.entries_before_retention, want.row_meta.entries_before_retention)
+        lo, hi = b.n // 3, b.n - 5
+        part = mc.compute_preconditioner(b, cfg, rows=(lo, hi))
+        out = {"row_ptr": np.empty(hi - lo + 1, np.int64), "col_idx": np.empty(part.m.nnz()),
+               "values": np.empty(part.m.nnz())}
+        out["col_idx"] = out["col_idx"].astype(np.int64)
+        got = mc.compute_preconditioner(b, cfg, out=out, rows=(lo, hi))
+        assert got.m == part.m
