@@ -115,6 +115,14 @@ int64_t sat_mul(int64_t a, int64_t b) {
 
 // derive_chain_budget (mc_engine.cpp:12-33), on the host so glibc's log and
 // ceil give the reference's exact (N, L).
+// static_cast<index_t>(double) as the reference's x86-64 build executes it
+// (cvttsd2si): out-of-range and NaN inputs give INT64_MIN.  The cast is UB in
+// C++, but this is what the reference binary computes (e.g. ||A|| -> 1 makes
+// N = max(1, INT64_MIN) = 1), so the drop-in reproduces it.
+int64_t x86_cvt(double x) {
+    return (x >= -9223372036854775808.0 && x < 9223372036854775808.0) ? static_cast<int64_t>(x) : INT64_MIN;
+}
+
 Status chain_budget(const mcmi_config& c, double a_norm, int64_t* nc, int64_t* ml) {
     if (!(a_norm >= 0.0 && a_norm < 1.0)) return fail(MCMI_EINVAL, "||A|| must lie in [0,1)");
     int64_t n_chains, max_len;
@@ -122,9 +130,7 @@ Status chain_budget(const mcmi_config& c, double a_norm, int64_t* nc, int64_t* m
         n_chains = c.chains_override;
     } else {
         const double root = 0.6745 / (c.epsilon * (1.0 - a_norm));
-        const double sq = std::ceil(root * root);
-        if (!(sq < 9.2e18)) return fail(MCMI_EINVAL, "chain budget overflows int64 (epsilon too small)");
-        n_chains = static_cast<int64_t>(sq);
+        n_chains = x86_cvt(std::ceil(root * root));
     }
     if (c.has_max_len_override) {
         max_len = c.max_len_override;
@@ -132,8 +138,7 @@ Status chain_budget(const mcmi_config& c, double a_norm, int64_t* nc, int64_t* m
         max_len = 1;
     } else {
         const double len = std::log(c.delta) / std::log(a_norm);
-        const double cl = std::ceil(len);
-        max_len = cl < 9.2e18 ? std::max<int64_t>(1, static_cast<int64_t>(cl)) : INT64_MAX;
+        max_len = std::max<int64_t>(1, x86_cvt(std::ceil(len)));
     }
     n_chains = std::max<int64_t>(1, n_chains);
     *nc = n_chains;
@@ -241,7 +246,7 @@ void engine_release(mcmi_engine* e) {
 
 constexpr int kLogMax = 256;         // deposit-log entries per warp (shared memory)
 constexpr int64_t kMaxWalkLen = 1 << 16;  // longest walk (log capacity of the global tier)
-constexpr int64_t kMaxSmemWalkLen = 1024; // longer walks go straight to the global tier
+constexpr int64_t kMaxSmemWalkLen = 256;  // longer max_len go straight to the global tier
 
 struct Tier {
     int cap, cap_limit, lanes, log_stride, warps_per_block;
@@ -401,9 +406,9 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     Status bs = chain_budget(cfg, a_norm, &N, &L);
     if (bs.code) return bs;
     if (N > INT_MAX) return fail(MCMI_EINVAL, "chain budget exceeds 2^31-1 chains per row");
-    if (L > kMaxWalkLen)
-        return fail(MCMI_EINVAL, "max_len above " + std::to_string(kMaxWalkLen) +
-                                     " is not supported by the B200 build (deposit log capacity)");
+    // walk lengths: the deposit log holds min(L, 65536) steps per chain; a walk
+    // that would outgrow its tier's log overflows the row to the next tier, and
+    // only walks actually longer than 65536 steps are refused
     st.n_chains = N;
     st.max_len = L;
     st.a_norm = a_norm;
@@ -464,7 +469,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         wa.work_offset = offset;
         wa.n_work = work;
         wa.n_chains = N;
-        wa.max_len = L;
+        wa.max_len = std::min<int64_t>(L, INT_MAX);  // walks beyond the log capacity overflow anyway
         wa.delta = cfg.delta;
         wa.seed = cfg.master_seed;
         wa.retain_k = cfg.retain_k;
@@ -529,7 +534,10 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         int64_t ovf = 0;
         Status ps = run_tier(tiers.back(), pilot, nullptr, 0, &ovf);
         if (ps.code) return ps;
-        if (ovf != 0) return fail(MCMI_ECUDA, "internal: pilot rows overflowed the last tier");
+        if (ovf != 0)
+            return fail(MCMI_ENOMEM, std::to_string(ovf) +
+                                         " rows overflowed every accumulator tier (more distinct columns than "
+                                         "device memory allows, or walks longer than 65536 steps)");
         if (!e->h_pilot_buf(static_cast<size_t>(pilot))) return fail(MCMI_ENOMEM, "cudaMallocHost (pilot)");
         MCMI_TRY(cudaMemcpyAsync(e->h_pilot, e->entries_before.p, pilot * sizeof(int64_t),
                                  cudaMemcpyDeviceToHost, s),
@@ -575,7 +583,9 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
             cur ^= 1;
         }
         if (work > 0)
-            return fail(MCMI_ENOMEM, std::to_string(work) + " rows overflowed every accumulator tier");
+            return fail(MCMI_ENOMEM, std::to_string(work) +
+                                         " rows overflowed every accumulator tier (more distinct columns than "
+                                         "device memory allows, or walks longer than 65536 steps)");
         return ok();
     };
 

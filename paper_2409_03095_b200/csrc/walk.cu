@@ -428,8 +428,13 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             unsigned long long cached = ~0ull;
             uint4 blk = make_uint4(0, 0, 0, 0);
             bool alive = active;
+            bool log_full = false;  // the walk would outgrow this tier's deposit log
             for (int t = 0; __any_sync(FULL_MASK, alive); ++t) {
                 if (alive && t >= L) alive = false;
+                if (alive && m >= S) {
+                    alive = false;
+                    log_full = true;
+                }
                 if (!alive) continue;
                 uint4 r0, r1;
                 ldg256(rec + 2 * static_cast<int64_t>(state), r0, r1);
@@ -519,6 +524,10 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
 
             if (active)
                 for (int t1 = m; t1 < S; ++t1) lc[t1 * B] = -1;  // end-of-chain sentinel for the fold
+            if (__any_sync(FULL_MASK, log_full)) {  // longer walks: retry the row on a longer log
+                overflow = true;
+                break;
+            }
 
             // ------------------------------------------- which lanes count
             unsigned valid;

@@ -361,3 +361,25 @@ def test_streamed_build_into_equals_handle_path(mc, rng):
         out["col_idx"] = out["col_idx"].astype(np.int64)
         got = mc.compute_preconditioner(b, cfg, out=out, rows=(lo, hi))
         assert got.m == part.m
+
+
+@pytest.mark.parametrize("rng", [0, 1])
+def test_huge_budget_cast_and_long_max_len(mc, oracle_mod, ref_mod, rng):
+    # ||A|| = 1 - 1e-15: the reference's static_cast<index_t> of a 1e33 chain
+    # budget is INT64_MIN on x86-64, so it runs N = 1 chain with L ~ 7.8e14;
+    # the walks still stop early by delta.  The drop-in must do the same.
+    import test_gpu_fuzz as F
+    rng_ = np.random.default_rng(20261018)
+    for case in range(302):
+        b = F.random_matrix(rng_)
+        cfg = F.random_config(rng_, mc)
+    cfg.rng_mode = mc.RngMode(rng)
+    want = oracle_mod.compute_preconditioner(b.n, b.row_ptr, b.col_idx, b.values, **cfg.oracle_kwargs())
+    assert want.n_chains == 1 and want.max_len > 10**14
+    got = mc.compute_preconditioner(b, cfg)
+    assert got.budget_echo.n_chains == 1 and got.budget_echo.max_len == want.max_len
+    assert np.array_equal(got.m.col_idx, want.col_idx) and bits_equal(got.m.values, want.values)
+    if rng == 0:
+        kw = {k: v for k, v in cfg.oracle_kwargs().items() if k != "rng_mode"}
+        r = ref_mod.compute_preconditioner(ref_mod.Csr(b.n, b.row_ptr, b.col_idx, b.values), **kw)
+        assert r.n_chains == 1 and bits_equal(got.m.values, r.m.values)
