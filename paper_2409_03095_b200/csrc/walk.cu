@@ -43,6 +43,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <type_traits>
 
 #include "common.cuh"
 #include "kernels.cuh"
@@ -343,6 +344,10 @@ constexpr int kRankTopkMax = 256;  // above this row length retain_top_k uses ra
 
 template <int MODE, int MINB, bool GL>
 __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
+    // MODE 0: reference stream with 32-bit draw positions (N*L < 2^32, every
+    // practical budget); MODE 2: the same with 64-bit positions; MODE 1: keyed.
+    constexpr bool IS_REF = MODE != 1;
+    using PosT = typename std::conditional<MODE == 2, unsigned long long, unsigned>::type;
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = static_cast<int>(threadIdx.x & 31);
     const int warp = static_cast<int>(threadIdx.x >> 5);
@@ -358,6 +363,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     const unsigned cap_mask = static_cast<unsigned>(cap - 1);
     const int shift = 32 - (31 - __clz(cap));
     const unsigned lt_mask = (1u << lane) - 1u;
+    const int s_shift = (S & (S - 1)) == 0 ? 31 - __clz(S) : -1;  // log2(S) when S is a power of two
 
     const uint4* __restrict__ rec = a.t.rec;
     const double2* __restrict__ ent = a.t.ent;
@@ -397,18 +403,18 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
         int chains_run = N;
         unsigned long long row_steps = 0, row_deg = 0;
         // reference-stream speculation state
-        unsigned long long D = 0;
+        PosT D = 0;
         unsigned ell = static_cast<unsigned>(a.ell0);
         bool row_done = false;
 
         while (!row_done) {
             // ------------------------------------------------ walk one batch
             bool active;
-            unsigned long long pos = 0;  // next draw index (reference stream)
+            PosT pos = 0;                // next draw index (reference stream)
             int chain = 0;               // chain index (keyed)
-            if (MODE == 0) {
+            if (IS_REF) {
                 active = lane < B;
-                pos = D + static_cast<unsigned long long>(lane) * ell;
+                pos = D + static_cast<PosT>(lane) * ell;
             } else {
                 chain = chains_done + lane;
                 active = lane < B && chain < N;
@@ -425,7 +431,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             double w = 1.0;
             unsigned draws = 0;
             unsigned lane_steps = 0, lane_deg = 0;  // committed only if this lane's chain counts
-            unsigned long long cached = ~0ull;
+            PosT cached = static_cast<PosT>(~0ull);
             uint4 blk = make_uint4(0, 0, 0, 0);
             bool alive = active;
             bool log_full = false;  // the walk would outgrow this tier's deposit log
@@ -452,11 +458,12 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                     nxt = static_cast<int>(r1.z);
                 } else {
                     double u;
-                    if (MODE == 0) {
-                        const unsigned long long b = pos >> 1;
+                    if (IS_REF) {
+                        const PosT b = pos >> 1;
                         if (b != cached) {
                             blk = philox4x32_10(
-                                make_uint4(static_cast<uint32_t>(b), static_cast<uint32_t>(b >> 32),
+                                make_uint4(static_cast<uint32_t>(b),
+                                           static_cast<uint32_t>(static_cast<unsigned long long>(b) >> 32),
                                            static_cast<uint32_t>(row),
                                            0u),  // row < 2^31: stream id high word
                                 key);
@@ -466,7 +473,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                                       : u32pair_to_double(blk.x, blk.y);
                         ++pos;
                     } else {
-                        const unsigned long long b = static_cast<unsigned>(t) >> 1;
+                        const PosT b = static_cast<unsigned>(t) >> 1;
                         if (b != cached) {
                             blk = philox4x32_10(
                                 make_uint4(static_cast<uint32_t>(b), static_cast<uint32_t>(chain),
@@ -539,9 +546,9 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 valid = 1u;
                 chains_run = 1;
                 row_done = true;
-            } else if (MODE == 0 && __all_sync(FULL_MASK, !active || draws == ell)) {
+            } else if (IS_REF && __all_sync(FULL_MASK, !active || draws == ell)) {
                 valid = __ballot_sync(FULL_MASK, active);  // every chain drew ell times: all on the orbit
-            } else if (MODE == 0) {
+            } else if (IS_REF) {
                 int nxtl = lane;
                 if (active && draws > 0) {
                     const unsigned q = draws / ell;
@@ -568,10 +575,10 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 row_steps += lane_steps;
                 row_deg += lane_deg;
             }
-            if (MODE == 0 && !row_done) {
+            if (IS_REF && !row_done) {
                 const int lv = 31 - __clz(valid);
                 const unsigned klv = __shfl_sync(FULL_MASK, draws, lv);
-                D = D + static_cast<unsigned long long>(lv) * ell + klv;
+                D = D + static_cast<PosT>(lv) * ell + klv;
                 // Next stride: prefix speculation (ell = chain 0's draws) yields
                 // ~1/p chains per window when a fraction p of chains draw a
                 // different count; dense candidates (ell = 1, every draw index)
@@ -642,8 +649,10 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             const int span = B * S;
             for (int base = 0; base < span; base += 32) {
                 const int p = base + lane;
-                // chain of position p: p / S (S == 1: the magic would be 2^32)
-                const int j = min(S == 1 ? p : static_cast<int>(__umulhi(static_cast<unsigned>(p), a.log_magic)), 31);
+                // chain of position p: p / S (shift for power-of-two S, else the magic multiply)
+                const int j = min(s_shift >= 0 ? (p >> s_shift)
+                                               : static_cast<int>(__umulhi(static_cast<unsigned>(p), a.log_magic)),
+                                  31);
                 bool ok = p < span && ((valid >> j) & 1u);
                 const int q = (p - j * S) * B + j;  // chain-major position p -> step-major slot
                 int c = ok ? sm.log_col[q] : -1;
@@ -872,6 +881,12 @@ cudaError_t launch_walk(const WalkArgs& a, int warps_per_block, int num_sms, boo
                                : launch_walk_t<1, 4, true>(a, warps_per_block, num_sms, max_warps, s);
     }
     const int mb = walk_minb();
+    const bool pos64 = static_cast<double>(a.n_chains) * static_cast<double>(std::max<int64_t>(a.max_len, 1)) >=
+                           4294967295.0 ||  // draw positions beyond 32 bits
+                       getenv("MCMI_FORCE_POS64") != nullptr;  // tests exercise the 64-bit variant
+    if (a.rng_mode == 0 && pos64)
+        return global_tier ? launch_walk_t<2, 4, true>(a, warps_per_block, num_sms, max_warps, s)
+                           : launch_walk_t<2, 6, false>(a, warps_per_block, num_sms, 0, s);
     if (a.rng_mode == 0) {
         if (mb == 5) return launch_walk_t<0, 5, false>(a, warps_per_block, num_sms, 0, s);
         if (mb == 6) return launch_walk_t<0, 6, false>(a, warps_per_block, num_sms, 0, s);

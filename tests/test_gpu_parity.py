@@ -383,3 +383,14 @@ def test_huge_budget_cast_and_long_max_len(mc, oracle_mod, ref_mod, rng):
         kw = {k: v for k, v in cfg.oracle_kwargs().items() if k != "rng_mode"}
         r = ref_mod.compute_preconditioner(ref_mod.Csr(b.n, b.row_ptr, b.col_idx, b.values), **kw)
         assert r.n_chains == 1 and bits_equal(got.m.values, r.m.values)
+
+
+@pytest.mark.parametrize("name", ["poisson2d_100_default_seed0", "rdb2048_acc6", "tridiag_longwalk"])
+def test_reference_stream_64bit_positions(mc, name, monkeypatch):
+    # budgets with N*L >= 2^32 draws per row use 64-bit draw positions; force
+    # that kernel variant on the goldens (the results must not change)
+    monkeypatch.setenv("MCMI_FORCE_POS64", "1")
+    case = GOLD[name]
+    b = _csr(mc, case["input"])
+    inv = mc.compute_preconditioner(b, _cfg(mc, case["config"]))
+    assert mm_sha256(b.n, inv.m.row_ptr, inv.m.col_idx, inv.m.values) == case["mm_sha256"]
