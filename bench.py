@@ -287,7 +287,14 @@ def run_ours(args):
     ms_local = ev0.elapsed_time(ev1) / max(args.steps, 1)
     steps_local = sum(s["walk_steps"] for s in stats) / max(args.steps, 1)
     walk_ms_local = sum(s["ms_walk_kernel"] for s in stats) / max(args.steps, 1)
-    alg_bytes_local = sum(20 * s["walk_steps"] + 8 * s["walk_deg_sum"] for s in stats) / max(args.steps, 1)
+    # algorithmic bytes per build: 20*steps + 8*sum deg(s); the
+    # sum of degrees comes from one extra, untimed build with MCMI_FLAG_DEG_STATS
+    # (identical walks, so the count is exact for every timed build)
+    dcfg = McConfig(**{k: getattr(cfg, k) for k in cfg.__dataclass_fields__})
+    dcfg.deg_stats = True
+    deg_sum = eng.build(b.n, d_rp, d_ci, d_v, dcfg, lo, hi, stream=stream).stats["walk_deg_sum"]
+    torch.cuda.synchronize()
+    alg_bytes_local = 20 * steps_local + 8 * deg_sum
     launches_local = sum(s["launches"] for s in stats)
     agg = torch.tensor([ms_local, steps_local, walk_ms_local, alg_bytes_local, launches_local],
                        dtype=torch.float64, device=device)

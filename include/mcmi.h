@@ -72,7 +72,13 @@ typedef struct mcmi_config {
     uint64_t master_seed;
     int32_t rng_mode; /* MCMI_RNG_*, default MCMI_RNG_REFERENCE */
     int32_t device;   /* CUDA device ordinal for mcmi_build */
+    int32_t flags;    /* MCMI_FLAG_*, default 0 */
+    int32_t reserved;
 } mcmi_config;
+
+/* flags */
+#define MCMI_FLAG_DEG_STATS 1 /* also count sum of deg(s) over walk steps (mcmi_stats.walk_deg_sum);
+                                 costs ~4% walk throughput (registers), so it is opt-in */
 
 /* Fills cfg with the reference defaults (McConfig{}). */
 void mcmi_config_default(mcmi_config* cfg);
@@ -96,7 +102,8 @@ typedef struct mcmi_stats {
     int64_t rows;         /* rows built (row_end - row_begin) */
     int64_t nnz;          /* entries of the built rows of M */
     int64_t walk_steps;   /* sampled transitions (one per s->t move) */
-    int64_t walk_deg_sum; /* sum over steps of deg(s): algorithmic bytes = 20*steps + 8*deg_sum */
+    int64_t walk_deg_sum; /* sum over steps of deg(s) (MCMI_FLAG_DEG_STATS, else -1):
+                             algorithmic bytes = 20*steps + 8*deg_sum */
     int64_t hash_cap;     /* accumulator capacity of the first tier */
     int64_t rows_retried; /* rows re-run on a larger accumulator tier */
     double ms_tables;     /* device time: drop + split + transition tables */

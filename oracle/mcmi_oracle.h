@@ -37,6 +37,8 @@ typedef struct orc_config {
     uint64_t master_seed;
     int32_t rng_mode; /* 0 reference stream, 1 keyed (row, chain, step) */
     int32_t device;   /* ignored */
+    int32_t flags;    /* ignored (the oracle always counts) */
+    int32_t reserved;
 } orc_config;
 
 typedef struct orc_result orc_result;

@@ -34,6 +34,8 @@ class OrcConfig(C.Structure):
         ("master_seed", C.c_uint64),
         ("rng_mode", C.c_int32),
         ("device", C.c_int32),
+        ("flags", C.c_int32),
+        ("reserved", C.c_int32),
     ]
 
 
@@ -71,7 +73,7 @@ def lib():
 def make_config(**kw) -> OrcConfig:
     c = OrcConfig(epsilon=0.0625, delta=0.0625, alpha=5.0, mode=1, drop_mode=0, drop_fraction=0.0,
                   retain_k=0, has_chains_override=0, has_max_len_override=0, chains_override=0,
-                  max_len_override=0, master_seed=0, rng_mode=0, device=0)
+                  max_len_override=0, master_seed=0, rng_mode=0, device=0, flags=0, reserved=0)
     for k, v in kw.items():
         if k == "chains_override":
             if v is not None:
@@ -79,6 +81,8 @@ def make_config(**kw) -> OrcConfig:
         elif k == "max_len_override":
             if v is not None:
                 c.has_max_len_override, c.max_len_override = 1, int(v)
+        elif k == "deg_stats":
+            continue
         else:
             setattr(c, k, v)
     return c

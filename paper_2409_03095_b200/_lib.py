@@ -40,7 +40,12 @@ class mcmi_config(C.Structure):
         ("master_seed", C.c_uint64),
         ("rng_mode", C.c_int32),
         ("device", C.c_int32),
+        ("flags", C.c_int32),
+        ("reserved", C.c_int32),
     ]
+
+
+MCMI_FLAG_DEG_STATS = 1
 
 
 class mcmi_csr_view(C.Structure):

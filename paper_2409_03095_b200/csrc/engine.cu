@@ -480,6 +480,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         wa.log_stride = t.log_stride;
         wa.log_magic = static_cast<unsigned>((0x100000000ull + t.log_stride - 1) / t.log_stride);
         wa.ell0 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(L, 2)));
+        wa.deg_stats = (cfg.flags & MCMI_FLAG_DEG_STATS) ? 1 : 0;
         wa.gscratch = nullptr;
         int64_t max_warps = 0;
         if (t.global) {
@@ -711,7 +712,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         }
     }
     st.walk_steps = static_cast<int64_t>(total_steps);
-    st.walk_deg_sum = static_cast<int64_t>(total_deg);
+    st.walk_deg_sum = (cfg.flags & MCMI_FLAG_DEG_STATS) ? static_cast<int64_t>(total_deg) : -1;
     MCMI_TRY(cudaEventRecord(e->ev[3], s), "cudaEventRecord");
     MCMI_TRY(cudaStreamSynchronize(s), "assembly");
     float t01 = 0, t12 = 0, t23 = 0, t03 = 0;

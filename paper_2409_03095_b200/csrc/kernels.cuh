@@ -85,6 +85,7 @@ struct WalkArgs {
     int log_stride;         // max(max_len, 1) step deposits per chain
     unsigned log_magic;     // ceil(2^32 / log_stride) for log_stride >= 2: p / S == __umulhi(p, magic)
     int ell0;               // initial speculative draw stride (reference-stream mode)
+    int deg_stats;          // count sum deg(s) (MCMI_FLAG_DEG_STATS)
     unsigned char* gscratch;  // global-tier per-warp accumulator + log (nullptr for smem tiers)
     // outputs, indexed by local row (row - row_begin)
     int* stage_col;

@@ -342,7 +342,7 @@ __device__ int sort_by_column(int* keys, double* vals, int s) {
 
 constexpr int kRankTopkMax = 256;  // above this row length retain_top_k uses radix_topk
 
-template <int MODE, int MINB, bool GL>
+template <int MODE, int MINB, bool GL, bool DEG>
 __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     // MODE 0: reference stream with 32-bit draw positions (N*L < 2^32, every
     // practical budget); MODE 2: the same with 64-bit positions; MODE 1: keyed.
@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                     continue;
                 }
                 ++lane_steps;
-                lane_deg += deg;
+                if (DEG) lane_deg += deg;
                 double ratio;
                 int nxt;
                 if (deg == 1) {  // forced move, no draw (mc_engine.cpp:69); inline in the record
@@ -841,16 +841,16 @@ size_t walk_global_bytes_per_warp(int cap, int lanes, int log_stride) {
     return walk_smem_bytes_per_warp(cap, lanes, log_stride);
 }
 
-template <int MODE, int MINB, bool GL>
+template <int MODE, int MINB, bool GL, bool DEG>
 cudaError_t launch_walk_t(const WalkArgs& a, int warps_per_block, int num_sms, int64_t max_warps,
                           cudaStream_t s) {
     const size_t smem = GL ? 0 : walk_smem_bytes_per_warp(a.cap, a.lanes, a.log_stride) * warps_per_block;
     const int threads = warps_per_block * 32;
-    cudaError_t e = cudaFuncSetAttribute(k_walk<MODE, MINB, GL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_walk<MODE, MINB, GL, DEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<MODE, MINB, GL>, threads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<MODE, MINB, GL, DEG>, threads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     int64_t blocks = static_cast<int64_t>(per_sm) * num_sms;
@@ -858,7 +858,7 @@ cudaError_t launch_walk_t(const WalkArgs& a, int warps_per_block, int num_sms, i
     if (blocks > need) blocks = need;
     if (max_warps > 0 && blocks * warps_per_block > max_warps)
         blocks = std::max<int64_t>(1, max_warps / warps_per_block);
-    k_walk<MODE, MINB, GL><<<static_cast<unsigned>(blocks), threads, smem, s>>>(a);
+    k_walk<MODE, MINB, GL, DEG><<<static_cast<unsigned>(blocks), threads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -876,25 +876,32 @@ int walk_minb() {
 cudaError_t launch_walk(const WalkArgs& a, int warps_per_block, int num_sms, bool global_tier,
                         int64_t max_warps, cudaStream_t s) {
     if (a.n_work <= 0) return cudaSuccess;
-    if (global_tier) {  // rare rows; occupancy is bounded by the scratch budget anyway
-        return a.rng_mode == 0 ? launch_walk_t<0, 4, true>(a, warps_per_block, num_sms, max_warps, s)
-                               : launch_walk_t<1, 4, true>(a, warps_per_block, num_sms, max_warps, s);
-    }
     const int mb = walk_minb();
     const bool pos64 = static_cast<double>(a.n_chains) * static_cast<double>(std::max<int64_t>(a.max_len, 1)) >=
                            4294967295.0 ||  // draw positions beyond 32 bits
                        getenv("MCMI_FORCE_POS64") != nullptr;  // tests exercise the 64-bit variant
-    if (a.rng_mode == 0 && pos64)
-        return global_tier ? launch_walk_t<2, 4, true>(a, warps_per_block, num_sms, max_warps, s)
-                           : launch_walk_t<2, 6, false>(a, warps_per_block, num_sms, 0, s);
-    if (a.rng_mode == 0) {
-        if (mb == 5) return launch_walk_t<0, 5, false>(a, warps_per_block, num_sms, 0, s);
-        if (mb == 6) return launch_walk_t<0, 6, false>(a, warps_per_block, num_sms, 0, s);
-        return launch_walk_t<0, 4, false>(a, warps_per_block, num_sms, 0, s);
+    const int mode = a.rng_mode == 0 ? (pos64 ? 2 : 0) : 1;
+    // variants: the global tier and the statistics build use one launch bound
+#define MCMI_WALK_RARE(M)                                                                              \
+    if (global_tier)                                                                                   \
+        return a.deg_stats ? launch_walk_t<M, 4, true, true>(a, warps_per_block, num_sms, max_warps, s) \
+                           : launch_walk_t<M, 4, true, false>(a, warps_per_block, num_sms, max_warps, s); \
+    if (a.deg_stats) return launch_walk_t<M, 6, false, true>(a, warps_per_block, num_sms, 0, s);
+    if (mode == 2) {
+        MCMI_WALK_RARE(2)
+        return launch_walk_t<2, 6, false, false>(a, warps_per_block, num_sms, 0, s);
     }
-    if (mb == 5) return launch_walk_t<1, 5, false>(a, warps_per_block, num_sms, 0, s);
-    if (mb == 6) return launch_walk_t<1, 6, false>(a, warps_per_block, num_sms, 0, s);
-    return launch_walk_t<1, 4, false>(a, warps_per_block, num_sms, 0, s);
+    if (mode == 0) {
+        MCMI_WALK_RARE(0)
+        if (mb == 5) return launch_walk_t<0, 5, false, false>(a, warps_per_block, num_sms, 0, s);
+        if (mb == 4) return launch_walk_t<0, 4, false, false>(a, warps_per_block, num_sms, 0, s);
+        return launch_walk_t<0, 6, false, false>(a, warps_per_block, num_sms, 0, s);
+    }
+    MCMI_WALK_RARE(1)
+    if (mb == 5) return launch_walk_t<1, 5, false, false>(a, warps_per_block, num_sms, 0, s);
+    if (mb == 4) return launch_walk_t<1, 4, false, false>(a, warps_per_block, num_sms, 0, s);
+    return launch_walk_t<1, 6, false, false>(a, warps_per_block, num_sms, 0, s);
+#undef MCMI_WALK_RARE
 }
 
 }  // namespace mcmi

@@ -73,6 +73,7 @@ class McConfig:  # mc_engine.hpp:15-26
     master_seed: int = 0
     rng_mode: RngMode = RngMode.reference
     device: int = 0
+    deg_stats: bool = False  #: also count sum deg(s) over steps (stats["walk_deg_sum"]); ~4% slower
 
     def to_c(self) -> L.mcmi_config:
         c = L.mcmi_config()
@@ -90,6 +91,7 @@ class McConfig:  # mc_engine.hpp:15-26
         c.master_seed = int(self.master_seed) & 0xFFFFFFFFFFFFFFFF
         c.rng_mode = int(self.rng_mode)
         c.device = int(self.device)
+        c.flags = L.MCMI_FLAG_DEG_STATS if self.deg_stats else 0
         return c
 
     def oracle_kwargs(self) -> dict:

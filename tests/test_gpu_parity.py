@@ -61,7 +61,7 @@ def test_reference_stream_byte_identical_to_reference(mc, name):
 def test_keyed_bit_identical_to_oracle(mc, oracle_mod, name):
     case = GOLD[name]
     b = _csr(mc, case["input"])
-    cfg = _cfg(mc, case["config"], rng_mode=1)
+    cfg = _cfg(mc, case["config"], rng_mode=1, deg_stats=True)
     inv = mc.compute_preconditioner(b, cfg)
     want = oracle_mod.compute_preconditioner(b.n, b.row_ptr, b.col_idx, b.values, **cfg.oracle_kwargs())
     assert np.array_equal(inv.m.row_ptr, want.row_ptr)
@@ -76,8 +76,9 @@ def test_keyed_bit_identical_to_oracle(mc, oracle_mod, name):
 @pytest.mark.parametrize("rng", [0, 1])
 def test_step_counters_match_oracle(mc, oracle_mod, rng):
     b = _csr(mc, "convdiff:100:0:0")
-    inv = mc.compute_preconditioner(b, mc.McConfig(rng_mode=rng))
+    inv = mc.compute_preconditioner(b, mc.McConfig(rng_mode=rng, deg_stats=True))
     want = oracle_mod.compute_preconditioner(b.n, b.row_ptr, b.col_idx, b.values, rng_mode=rng)
+    assert mc.compute_preconditioner(b, mc.McConfig(rng_mode=rng)).stats["walk_deg_sum"] == -1  # opt-in
     assert inv.stats["walk_steps"] == want.walk_steps
     if rng == 0:
         assert want.walk_steps == 2819436  # SURVEY.md §6 probe of the reference
