@@ -161,7 +161,7 @@ struct mcmi_engine {
     DevBuf gscratch;  // global accumulator tier
     DevBuf out_rp, out_col, out_val;
     // streamed build (mcmi_build_into): double-buffered output slabs + copy stream
-    DevBuf rp_slab[2], col_slab[2], val_slab[2];
+    DevBuf col_slab[2], val_slab[2];
     cudaStream_t copy = nullptr;
     cudaEvent_t copy_done[2] = {};
     cudaEvent_t chunk_ready = nullptr;
@@ -180,7 +180,6 @@ struct mcmi_engine {
     int64_t* h_i64 = nullptr;             // pinned [4]
     int64_t* h_pilot = nullptr;           // pinned pilot-row RowMeta
     size_t h_pilot_n = 0;
-    mcmi_device_csr last{};
     int64_t* h_pilot_buf(size_t count) {
         if (count > h_pilot_n) {
             if (h_pilot) cudaFreeHost(h_pilot);
@@ -228,7 +227,7 @@ void engine_release(mcmi_engine* e) {
                       &e->colA, &e->b1, &e->scan_tmp, &e->cq_tmp, &e->stage_col, &e->stage_val,
                       &e->row_cnt, &e->row_src, &e->chains_used, &e->entries_before,
                       &e->counters, &e->ovf[0], &e->ovf[1], &e->gscratch, &e->out_rp, &e->out_col,
-                      &e->out_val, &e->rp_slab[0], &e->rp_slab[1], &e->col_slab[0], &e->col_slab[1],
+                      &e->out_val, &e->col_slab[0], &e->col_slab[1],
                       &e->val_slab[0], &e->val_slab[1]})
         b->release();
     for (auto& ev : e->copy_done)
@@ -640,11 +639,11 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
             if (ws.code) return ws;
             if (dbg) cudaEventRecord(dev[4 * c + 1], s);
             const int64_t cr = hi - lo;
-            int64_t* rp_slab = e->out_rp.as<int64_t>() + lo;  // chunk-local offsets, then global
+            int64_t* rp_chunk = e->out_rp.as<int64_t>() + lo;  // chunk-local offsets, then global
             // wait until chunk c-2's copies released this slab pair
             MCMI_TRY(cudaStreamWaitEvent(s, e->copy_done[c & 1], 0), "wait copy");
-            MCMI_TRY(scan_rows_exclusive(e->row_cnt.as<int>() + lo, rp_slab, cr, e->scan_tmp.p, s), "scan rows");
-            MCMI_TRY(cudaMemcpyAsync(e->h_i64, rp_slab + cr, sizeof(int64_t), cudaMemcpyDeviceToHost, s),
+            MCMI_TRY(scan_rows_exclusive(e->row_cnt.as<int>() + lo, rp_chunk, cr, e->scan_tmp.p, s), "scan rows");
+            MCMI_TRY(cudaMemcpyAsync(e->h_i64, rp_chunk + cr, sizeof(int64_t), cudaMemcpyDeviceToHost, s),
                      "read chunk nnz");
             MCMI_TRY(cudaStreamSynchronize(s), "scan rows");
             const int64_t cn = e->h_i64[0];
@@ -661,10 +660,10 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
                 int64_t* cs = e->col_slab[c & 1].as<int64_t>();
                 double* vs = e->val_slab[c & 1].as<double>();
                 MCMI_TRY(launch_compact(e->stage_col.as<int>(), e->stage_val.as<double>(),
-                                        e->row_src.as<int64_t>() + lo, e->row_cnt.as<int>() + lo, rp_slab, cr, cs,
+                                        e->row_src.as<int64_t>() + lo, e->row_cnt.as<int>() + lo, rp_chunk, cr, cs,
                                         vs, s),
                          "compact");
-                MCMI_TRY(launch_add_offset(rp_slab, running, cr, s), "row_ptr offset");
+                MCMI_TRY(launch_add_offset(rp_chunk, running, cr, s), "row_ptr offset");
                 MCMI_TRY(cudaEventRecord(e->chunk_ready, s), "cudaEventRecord");
                 MCMI_TRY(cudaStreamWaitEvent(e->copy, e->chunk_ready, 0), "wait chunk");
                 if (dbg) cudaEventRecord(dev[4 * c + 2], e->copy);
@@ -734,7 +733,6 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     out->values = e->out_val.as<double>();
     out->chains_used = e->chains_used.as<int64_t>();
     out->entries_before = e->entries_before.as<int64_t>();
-    e->last = *out;
     if (stats) *stats = st;
     return ok();
 }
@@ -766,6 +764,41 @@ mcmi_engine* acquire_engine(int device, Status* st) {
 void release_engine(mcmi_engine* e) {
     std::lock_guard<std::mutex> lk(g_cache_mu);
     g_cache.push_back(e);
+}
+
+// Host CSR in: stage B on the engine's stream (stream-ordered pool allocations,
+// cached across calls), build rows [row_begin, row_end), release the staging.
+Status build_from_host(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& cfg, int64_t row_begin,
+                       int64_t row_end, mcmi_device_csr* dc, mcmi_stats* stats, const HostSink* sink) {
+    const int64_t n = b.n;
+    if (n < 0) return fail(MCMI_EINVAL, "negative dimension");
+    if (n > 0 && !b.row_ptr) return fail(MCMI_EINVAL, "null row_ptr");
+    const int64_t nnz = n > 0 ? b.row_ptr[n] : 0;
+    if (nnz < 0) return fail(MCMI_EINVAL, "row_ptr[n] is negative");
+    if (nnz > 0 && (!b.col_idx || !b.values)) return fail(MCMI_EINVAL, "null col_idx / values");
+    MCMI_TRY(cudaSetDevice(e->device), "cudaSetDevice");
+    cudaStream_t s = e->own;
+    void *d_rp = nullptr, *d_ci = nullptr, *d_v = nullptr;
+    MCMI_TRY(cudaMallocAsync(&d_rp, (n + 1) * sizeof(int64_t), s), "alloc B");
+    MCMI_TRY(cudaMallocAsync(&d_ci, std::max<int64_t>(nnz, 1) * sizeof(int64_t), s), "alloc B");
+    MCMI_TRY(cudaMallocAsync(&d_v, std::max<int64_t>(nnz, 1) * sizeof(double), s), "alloc B");
+    Status st;
+    auto h2d = [&](void* dst, const void* src, size_t bytes) {
+        if (st.code == MCMI_OK && bytes)
+            st = cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s), "H2D");
+    };
+    h2d(d_rp, b.row_ptr, (n + 1) * sizeof(int64_t));
+    h2d(d_ci, b.col_idx, nnz * sizeof(int64_t));
+    h2d(d_v, b.values, nnz * sizeof(double));
+    if (st.code == MCMI_OK) {
+        const mcmi_csr_view dv{n, static_cast<int64_t*>(d_rp), static_cast<int64_t*>(d_ci),
+                               static_cast<double*>(d_v)};
+        st = engine_build(e, dv, cfg, row_begin, row_end, s, dc, stats, sink);
+    }
+    cudaFreeAsync(d_rp, s);
+    cudaFreeAsync(d_ci, s);
+    cudaFreeAsync(d_v, s);
+    return st;
 }
 
 }  // namespace
@@ -839,49 +872,28 @@ int mcmi_build_rows(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_
     Status st;
     mcmi_engine* e = acquire_engine(cfg->device, &st);
     if (!e) return report(st, err, errlen);
-    auto run = [&]() -> Status {
-        const int64_t n = b->n;
-        if (n < 0) return fail(MCMI_EINVAL, "negative dimension");
-        const int64_t nnz = n > 0 ? b->row_ptr[n] : 0;
-        cudaStream_t s = e->own;
-        // input staging: reuse engine-owned device buffers (grow-only)
-        void *d_rp = nullptr, *d_ci = nullptr, *d_v = nullptr;
-        MCMI_TRY(cudaMallocAsync(&d_rp, (std::max<int64_t>(n, 0) + 1) * sizeof(int64_t), s), "alloc B");
-        MCMI_TRY(cudaMallocAsync(&d_ci, std::max<int64_t>(nnz, 1) * sizeof(int64_t), s), "alloc B");
-        MCMI_TRY(cudaMallocAsync(&d_v, std::max<int64_t>(nnz, 1) * sizeof(double), s), "alloc B");
-        MCMI_TRY(cudaMemcpyAsync(d_rp, b->row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDefault, s), "H2D");
-        if (nnz > 0) {
-            MCMI_TRY(cudaMemcpyAsync(d_ci, b->col_idx, nnz * sizeof(int64_t), cudaMemcpyDefault, s), "H2D");
-            MCMI_TRY(cudaMemcpyAsync(d_v, b->values, nnz * sizeof(double), cudaMemcpyDefault, s), "H2D");
-        }
-        mcmi_csr_view dv{n, static_cast<int64_t*>(d_rp), static_cast<int64_t*>(d_ci),
-                         static_cast<double*>(d_v)};
-        mcmi_device_csr dc{};
-        mcmi_stats stats{};
-        Status bst = engine_build(e, dv, *cfg, row_begin, row_end, s, &dc, &stats);
-        cudaFreeAsync(d_rp, s);
-        cudaFreeAsync(d_ci, s);
-        cudaFreeAsync(d_v, s);
-        if (bst.code) return bst;
-        auto* r = new mcmi_result();
-        r->device = e->device;
-        r->n = dc.row_end - dc.row_begin;
-        r->nnz = dc.nnz;
-        r->n_chains = stats.n_chains;
-        r->max_len = stats.max_len;
-        r->stats = stats;
-        r->engine = e;
-        r->rp = dc.row_ptr;
-        r->ci = dc.col_idx;
-        r->v = dc.values;
-        r->cu = dc.chains_used;
-        r->eb = dc.entries_before;
-        *out = r;
-        return ok();
-    };
-    st = run();
-    if (st.code) release_engine(e);  // on success the result owns the engine until freed
-    return report(st, err, errlen);
+    mcmi_device_csr dc{};
+    mcmi_stats stats{};
+    st = build_from_host(e, *b, *cfg, row_begin, row_end, &dc, &stats, nullptr);
+    if (st.code) {
+        release_engine(e);
+        return report(st, err, errlen);
+    }
+    auto* r = new mcmi_result();  // owns the engine (and its output buffers) until freed
+    r->device = e->device;
+    r->n = dc.row_end - dc.row_begin;
+    r->nnz = dc.nnz;
+    r->n_chains = stats.n_chains;
+    r->max_len = stats.max_len;
+    r->stats = stats;
+    r->engine = e;
+    r->rp = dc.row_ptr;
+    r->ci = dc.col_idx;
+    r->v = dc.values;
+    r->cu = dc.chains_used;
+    r->eb = dc.entries_before;
+    *out = r;
+    return MCMI_OK;
 }
 
 int mcmi_build_into(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_begin, int64_t row_end,
@@ -893,34 +905,12 @@ int mcmi_build_into(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_
     Status st;
     mcmi_engine* e = acquire_engine(cfg->device, &st);
     if (!e) return report(st, err, errlen);
-    auto run = [&]() -> Status {
-        const int64_t n = b->n;
-        if (n < 0) return fail(MCMI_EINVAL, "negative dimension");
-        const int64_t bnnz = n > 0 ? b->row_ptr[n] : 0;
-        cudaStream_t s = e->own;
-        void *d_rp = nullptr, *d_ci = nullptr, *d_v = nullptr;
-        MCMI_TRY(cudaMallocAsync(&d_rp, (std::max<int64_t>(n, 0) + 1) * sizeof(int64_t), s), "alloc B");
-        MCMI_TRY(cudaMallocAsync(&d_ci, std::max<int64_t>(bnnz, 1) * sizeof(int64_t), s), "alloc B");
-        MCMI_TRY(cudaMallocAsync(&d_v, std::max<int64_t>(bnnz, 1) * sizeof(double), s), "alloc B");
-        MCMI_TRY(cudaMemcpyAsync(d_rp, b->row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDefault, s), "H2D");
-        if (bnnz > 0) {
-            MCMI_TRY(cudaMemcpyAsync(d_ci, b->col_idx, bnnz * sizeof(int64_t), cudaMemcpyDefault, s), "H2D");
-            MCMI_TRY(cudaMemcpyAsync(d_v, b->values, bnnz * sizeof(double), cudaMemcpyDefault, s), "H2D");
-        }
-        const mcmi_csr_view dv{n, static_cast<int64_t*>(d_rp), static_cast<int64_t*>(d_ci),
-                               static_cast<double*>(d_v)};
-        HostSink sink{row_ptr, col_idx, values, capacity, chains_used, entries_before};
-        mcmi_device_csr dc{};
-        mcmi_stats ls{};
-        Status bst = engine_build(e, dv, *cfg, row_begin, row_end, s, &dc, &ls, &sink);
-        cudaFreeAsync(d_rp, s);
-        cudaFreeAsync(d_ci, s);
-        cudaFreeAsync(d_v, s);
-        *nnz = ls.nnz;
-        if (stats) *stats = ls;
-        return bst;
-    };
-    st = run();
+    const HostSink sink{row_ptr, col_idx, values, capacity, chains_used, entries_before};
+    mcmi_device_csr dc{};
+    mcmi_stats ls{};
+    st = build_from_host(e, *b, *cfg, row_begin, row_end, &dc, &ls, &sink);
+    *nnz = ls.nnz;
+    if (stats) *stats = ls;
     release_engine(e);
     return report(st, err, errlen);
 }

@@ -20,10 +20,7 @@ struct Reductions {
     long long bad_col_row;           // first row holding a column outside [0,n), else LLONG_MAX
     unsigned long long max_deg;      // max row length of A
     unsigned long long a_nnz;        // entries of A
-    unsigned long long cq_threshold_bits;  // count-quantile: |v| of the n_drop-th smallest
-    long long cq_tie_budget;               // count-quantile: ties at the threshold to drop
-    long long bad_rowptr_row;              // first row with an invalid row_ptr, else LLONG_MAX
-    unsigned long long pad[5];
+    long long bad_rowptr_row;        // first row with an invalid row_ptr, else LLONG_MAX
 };
 
 // Transition tables (subsystem 1), one 32-byte record per state s:
