@@ -106,7 +106,8 @@ def load(path: str | None = None):
     global _lib
     if _lib is not None:
         return _lib
-    path = path or LIB
+    # MCMI_LIB_PATH: an alternative build of the same library (A/B kernel experiments)
+    path = path or os.environ.get("MCMI_LIB_PATH") or LIB
     if not os.path.exists(path):
         raise ImportError(
             f"{path} not found: the CUDA library is required (run `python -m paper_2409_03095_b200.build`)")

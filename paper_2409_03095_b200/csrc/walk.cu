@@ -81,24 +81,56 @@ __device__ __forceinline__ void ldg256(const void* p, uint4& lo, uint4& hi) {
                  : "l"(p));
 }
 
-// Insert-or-find; returns the slot or -1 if the table is full.
+// Insert-or-find; returns the slot or -1 if the table is full.  The key's home
+// slot h is probed first (one 4-byte load: most lookups end there, hit or
+// empty); past an occupied home slot the probe continues over 4-slot buckets
+// starting at h's bucket, one 16-byte load per bucket, slots in order.  A key
+// therefore sits in the first slot of that sequence that was empty when it was
+// inserted (no deletions while a row is open): an empty home slot or a bucket
+// holding an empty slot ends an unsuccessful search.  Concurrent inserts of
+// distinct keys (one leader per column in a fold chunk) race only through the
+// CAS; the loser re-reads.
+template <bool GL>
 __device__ __forceinline__ int hash_slot(int* keys, unsigned mask, int shift, int col,
                                          int& n_new) {
-    unsigned h = (static_cast<unsigned>(col) * 0x9E3779B1u) >> shift;
+    const unsigned h = (static_cast<unsigned>(col) * 0x9E3779B1u) >> shift;
     volatile int* vk = keys;
-    if (vk[h] == col) return static_cast<int>(h);  // common case: already present, no collision
-    for (unsigned probe = 0; probe <= mask; ++probe) {
-        const int k = vk[h];
-        if (k == col) return static_cast<int>(h);
-        if (k == EMPTY_KEY) {
-            const int old = atomicCAS(&keys[h], EMPTY_KEY, col);
+    const int kh = vk[h];
+    if (kh == col) return static_cast<int>(h);
+    if (kh == EMPTY_KEY) {
+        const int old = atomicCAS(&keys[h], EMPTY_KEY, col);
+        if (old == EMPTY_KEY) {
+            ++n_new;
+            return static_cast<int>(h);
+        }
+        if (old == col) return static_cast<int>(h);
+    }
+    unsigned b = h & ~3u;
+    for (unsigned visited = 0; visited <= mask;) {
+        int4 k4;
+        if (GL)
+            asm volatile("ld.volatile.global.v4.s32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(k4.x), "=r"(k4.y), "=r"(k4.z), "=r"(k4.w)
+                         : "l"(keys + b));
+        else
+            asm volatile("ld.volatile.shared.v4.s32 {%0,%1,%2,%3}, [%4];"
+                         : "=r"(k4.x), "=r"(k4.y), "=r"(k4.z), "=r"(k4.w)
+                         : "r"(static_cast<unsigned>(__cvta_generic_to_shared(keys + b))));
+        if (k4.x == col) return static_cast<int>(b);
+        if (k4.y == col) return static_cast<int>(b + 1);
+        if (k4.z == col) return static_cast<int>(b + 2);
+        if (k4.w == col) return static_cast<int>(b + 3);
+        const int e = k4.x == EMPTY_KEY ? 0 : k4.y == EMPTY_KEY ? 1 : k4.z == EMPTY_KEY ? 2 : k4.w == EMPTY_KEY ? 3 : 4;
+        if (e < 4) {
+            const int old = atomicCAS(&keys[b + e], EMPTY_KEY, col);
             if (old == EMPTY_KEY) {
                 ++n_new;
-                return static_cast<int>(h);
+                return static_cast<int>(b + e);
             }
-            if (old == col) return static_cast<int>(h);
+            continue;  // another leader took the slot: re-read the bucket
         }
-        h = (h + 1) & mask;
+        b = (b + 4) & mask;
+        visited += 4;
     }
     return -1;
 }
@@ -393,7 +425,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
         // the diagonal column's slot; its sum lives in a register (acc_r)
         int n_new0 = 0;
         int slot_r = 0;
-        if (lane == 0) slot_r = hash_slot(sm.keys, cap_mask, shift, rowc, n_new0);
+        if (lane == 0) slot_r = hash_slot<GL>(sm.keys, cap_mask, shift, rowc, n_new0);
         slot_r = __shfl_sync(FULL_MASK, slot_r, 0);
         double acc_r = 0.0;
 
@@ -669,7 +701,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 const int leader = __ffs(peers) - 1;
                 int slot = 0;
                 if (ok && rank == 0) {
-                    slot = hash_slot(sm.keys, cap_mask, shift, c, n_new);
+                    slot = hash_slot<GL>(sm.keys, cap_mask, shift, c, n_new);
                     if (slot < 0) fail = true;
                 }
                 slot = __shfl_sync(FULL_MASK, slot, leader);
