@@ -16,7 +16,7 @@
 #include <string>
 #include <vector>
 
-#include "../../include/mcmi.h"
+#include "mcmi.h"
 #include "kernels.cuh"
 
 using namespace mcmi;

@@ -6,7 +6,7 @@
 
 #include <cuda_runtime.h>
 
-#include "../../include/mcmi.h"
+#include "mcmi.h"
 
 namespace mcmi {
 

@@ -17,7 +17,7 @@
 #include <string>
 #include <vector>
 
-#include "../../include/mcmi.h"
+#include "mcmi.h"
 #include "common.cuh"
 #include "kernels.cuh"
 
