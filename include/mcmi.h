@@ -43,6 +43,8 @@ extern "C" {
 #define MCMI_ECUDA 4   /* CUDA runtime failure */
 #define MCMI_ENOMEM 5  /* device or host allocation failure */
 #define MCMI_ENODEV 6  /* no CUDA device / device ordinal invalid */
+#define MCMI_EPARSE 7  /* mcspai::ParseError (matrix_market.hpp:12-14), message names the line */
+#define MCMI_EIO 8     /* std::runtime_error from file I/O (cannot open / write failure) */
 
 /* AugmentationMode (split.hpp:9-12) */
 #define MCMI_AUGMENT_PLAIN 0
@@ -213,6 +215,32 @@ int mcmi_copy(void* dst, const void* src, size_t bytes, void* stream);
  * the device->host copies run asynchronously at full PCIe bandwidth. */
 int mcmi_host_register(void* ptr, size_t bytes);
 int mcmi_host_unregister(void* ptr);
+
+/* ------------------------------- Matrix Market I/O and triplets (§8f rank 2) */
+
+/* Host CSR owned by the library (parse / from_triplets output).  The arrays are
+ * borrowed through mcmi_host_csr_get and stay valid until mcmi_host_csr_free. */
+typedef struct mcmi_host_csr mcmi_host_csr;
+
+/* mcspai::CsrMatrix::from_triplets (csr.cpp:17-58): sort by (row, col), sum
+ * duplicates in the reference's sort order, prune exact zeros.  Errors:
+ * MCMI_ERANGE "triplet index out of range".  rows/cols/vals hold `count`
+ * entries (the reference's equal-length check lives in the caller's binding). */
+int mcmi_from_triplets(int64_t n, const int64_t* rows, const int64_t* cols, const double* vals,
+                       int64_t count, mcmi_host_csr** out, char* err, size_t errlen);
+/* mcspai::parse_matrix_market (matrix_market.cpp:27-147) over `len` bytes of
+ * text; MCMI_EPARSE errors carry the reference's "matrix market: line N: ..." */
+int mcmi_mm_parse(const char* text, size_t len, mcmi_host_csr** out, char* err, size_t errlen);
+/* mcspai::read_matrix_market_file (matrix_market.cpp:149-153) */
+int mcmi_mm_read_file(const char* path, mcmi_host_csr** out, char* err, size_t errlen);
+void mcmi_host_csr_get(const mcmi_host_csr* m, mcmi_csr_view* view);
+void mcmi_host_csr_free(mcmi_host_csr* m);
+/* mcspai::write_matrix_market (matrix_market.cpp:155-169): the same bytes
+ * ("%lld %lld %.17g" lines).  buf == NULL: *len = bytes needed, MCMI_OK;
+ * cap < needed: *len = needed, MCMI_ENOMEM. */
+int mcmi_mm_format(const mcmi_csr_view* m, char* buf, size_t cap, size_t* len, char* err, size_t errlen);
+/* mcspai::write_matrix_market_file (matrix_market.cpp:171-177) */
+int mcmi_mm_write_file(const mcmi_csr_view* m, const char* path, char* err, size_t errlen);
 
 /* Library identification: returns "mcmi <abi> sm_100a". */
 const char* mcmi_version(void);

@@ -18,10 +18,20 @@
 // Errors are re-thrown as the reference throws them: std::invalid_argument
 // (csr.cpp:129, split.cpp:48, mc_engine.cpp:14), SplitErrorT (split.cpp:68,95),
 // std::out_of_range (bad column index), std::runtime_error (CUDA / device).
+//
+// §8f rank 2, the formats either side of the build (same results byte for byte):
+//   from_triplets<CsrMatrix>(n, rows, cols, vals)            csr.cpp:17-58
+//   parse_matrix_market<CsrMatrix, ParseError>(istream&)     matrix_market.cpp:27-147
+//   read_matrix_market_file<CsrMatrix, ParseError>(path)     matrix_market.cpp:149-153
+//   write_matrix_market(m, ostream&)                         matrix_market.cpp:155-169
+//   write_matrix_market_file(m, path)                        matrix_market.cpp:171-177
 #ifndef MCMI_MCSPAI_COMPAT_HPP
 #define MCMI_MCSPAI_COMPAT_HPP
 
 #include <cstdint>
+#include <istream>
+#include <iterator>
+#include <ostream>
 #include <new>
 #include <stdexcept>
 #include <string>
@@ -106,6 +116,98 @@ ApproxInverseT compute_preconditioner(const CsrT& b, const CfgT& cfg, const Opti
     out.budget_echo.max_len = max_len;
     out.seed_echo = cfg.master_seed;
     return out;
+}
+
+namespace detail {
+
+template <class CsrT>
+mcmi_csr_view view_of(const CsrT& m) {
+    return mcmi_csr_view{static_cast<int64_t>(m.n), reinterpret_cast<const int64_t*>(m.row_ptr.data()),
+                         reinterpret_cast<const int64_t*>(m.col_idx.data()), m.values.data()};
+}
+
+template <class CsrT>
+CsrT take(mcmi_host_csr* h) {
+    mcmi_csr_view v;
+    mcmi_host_csr_get(h, &v);
+    CsrT m;
+    m.n = v.n;
+    const int64_t nnz = v.n > 0 ? v.row_ptr[v.n] : 0;
+    m.row_ptr.assign(v.row_ptr, v.row_ptr + (v.n > 0 ? v.n + 1 : 0));
+    if (v.n <= 0) m.row_ptr.assign(1, 0);
+    m.col_idx.assign(v.col_idx, v.col_idx + nnz);
+    m.values.assign(v.values, v.values + nnz);
+    mcmi_host_csr_free(h);
+    return m;
+}
+
+template <class ParseErrorT>
+[[noreturn]] inline void rethrow_io(int code, const char* msg) {
+    switch (code) {
+        case MCMI_EPARSE: throw ParseErrorT(msg);
+        case MCMI_EINVAL: throw std::invalid_argument(msg);
+        case MCMI_ERANGE: throw std::out_of_range(msg);
+        case MCMI_ENOMEM: throw std::bad_alloc();
+        default: throw std::runtime_error(msg);
+    }
+}
+
+}  // namespace detail
+
+template <class CsrT, class IndexVec, class ValueVec>
+CsrT from_triplets(int64_t n, const IndexVec& rows, const IndexVec& cols, const ValueVec& vals) {
+    if (rows.size() != cols.size() || rows.size() != vals.size())  // csr.cpp:20-21
+        throw std::invalid_argument("triplet arrays must have equal length");
+    char err[512] = {0};
+    mcmi_host_csr* h = nullptr;
+    const int code = mcmi_from_triplets(n, reinterpret_cast<const int64_t*>(rows.data()),
+                                        reinterpret_cast<const int64_t*>(cols.data()), vals.data(),
+                                        static_cast<int64_t>(rows.size()), &h, err, sizeof err);
+    if (code != MCMI_OK) detail::rethrow_io<std::runtime_error>(code, err);
+    return detail::take<CsrT>(h);
+}
+
+template <class CsrT, class ParseErrorT>
+CsrT parse_matrix_market(std::istream& in) {
+    const std::string text{std::istreambuf_iterator<char>(in), std::istreambuf_iterator<char>()};
+    char err[512] = {0};
+    mcmi_host_csr* h = nullptr;
+    const int code = mcmi_mm_parse(text.data(), text.size(), &h, err, sizeof err);
+    if (code != MCMI_OK) detail::rethrow_io<ParseErrorT>(code, err);
+    return detail::take<CsrT>(h);
+}
+
+template <class CsrT, class ParseErrorT>
+CsrT read_matrix_market_file(const std::string& path) {
+    char err[512] = {0};
+    mcmi_host_csr* h = nullptr;
+    const int code = mcmi_mm_read_file(path.c_str(), &h, err, sizeof err);
+    if (code != MCMI_OK) detail::rethrow_io<ParseErrorT>(code, err);
+    return detail::take<CsrT>(h);
+}
+
+template <class CsrT>
+void write_matrix_market(const CsrT& m, std::ostream& out) {
+    const mcmi_csr_view v = detail::view_of(m);
+    char err[512] = {0};
+    size_t len = 0;
+    std::string buf(static_cast<size_t>(128 + 48 * m.values.size()), '\0');
+    int code = mcmi_mm_format(&v, buf.data(), buf.size(), &len, err, sizeof err);
+    if (code == MCMI_ENOMEM && len > buf.size()) {
+        buf.resize(len);
+        code = mcmi_mm_format(&v, buf.data(), buf.size(), &len, err, sizeof err);
+    }
+    if (code != MCMI_OK) detail::rethrow_io<std::runtime_error>(code, err);
+    out.write(buf.data(), static_cast<std::streamsize>(len));
+    if (!out) throw std::runtime_error("matrix market: write failure");
+}
+
+template <class CsrT>
+void write_matrix_market_file(const CsrT& m, const std::string& path) {
+    const mcmi_csr_view v = detail::view_of(m);
+    char err[512] = {0};
+    const int code = mcmi_mm_write_file(&v, path.c_str(), err, sizeof err);
+    if (code != MCMI_OK) detail::rethrow_io<std::runtime_error>(code, err);
 }
 
 }  // namespace compat

@@ -4,10 +4,16 @@
 // with the unmodified reference (mcspai::compute_preconditioner_serial) and
 // once through include/mcmi/mcspai_compat.hpp (the B200 build), and requires
 // `serial.m == b200.m` (CsrMatrix::operator==, csr.hpp:39) plus equal RowMeta
-// and budget.  Exit 0 = byte-identical on every case.
+// and budget.  Also swaps the Matrix Market functions and from_triplets
+// (§8f rank 2) and requires identical bytes / matrices / exception types.
+// `dropin_demo --io-only` runs only those (no GPU needed).
+// Exit 0 = byte-identical on every case.
 #include <cstdio>
+#include <cstring>
+#include <sstream>
 
 #include "mcmi/mcspai_compat.hpp"
+#include "mcspai/matrix_market.hpp"
 #include "mcspai/mc_engine.hpp"
 #include "mcspai/synthetic.hpp"
 
@@ -26,8 +32,51 @@ static bool run(const char* name, const CsrMatrix& b, const McConfig& cfg) {
     return ok;
 }
 
-int main() {
+static bool io_case(const char* name, const CsrMatrix& m) {
+    std::ostringstream a, b;
+    write_matrix_market(m, a);                      // reference
+    mcmi::compat::write_matrix_market(m, b);        // B200 library
+    bool ok = a.str() == b.str();
+    std::istringstream in1(a.str()), in2(a.str());
+    const CsrMatrix p1 = parse_matrix_market(in1);
+    const CsrMatrix p2 = mcmi::compat::parse_matrix_market<CsrMatrix, ParseError>(in2);
+    ok = ok && p1 == p2 && p2 == m;
+    std::printf("[%s] mm %-19s n=%lld nnz=%lld bytes=%zu\n", ok ? "PASS" : "FAIL", name,
+                static_cast<long long>(m.n), static_cast<long long>(m.nnz()), b.str().size());
+    return ok;
+}
+
+static bool io_checks() {
     bool ok = true;
+    ok &= io_case("identity8", CsrMatrix::identity(8));
+    ok &= io_case("broad1024", make_broad_spectrum(1024, 24, 1e-4, 1.0, 7));
+    ok &= io_case("convdiff64", make_convection_diffusion(64, 20.0, 10.0));
+    // duplicates summed in the reference's sort order (3+ repeats of a coordinate)
+    std::vector<index_t> r, c;
+    std::vector<double> v;
+    for (int k = 0; k < 5000; ++k) {
+        r.push_back(k % 7);
+        c.push_back((k * 31) % 5);
+        v.push_back(1.0 / (k + 1) - 0.001 * (k % 13));
+    }
+    const CsrMatrix t1 = CsrMatrix::from_triplets(7, r, c, v);
+    const CsrMatrix t2 = mcmi::compat::from_triplets<CsrMatrix>(7, r, c, v);
+    std::printf("[%s] from_triplets with repeated coordinates\n", t1 == t2 ? "PASS" : "FAIL");
+    ok &= t1 == t2;
+    std::istringstream bad("%%MatrixMarket matrix coordinate real general\n2 3 1\n1 1 1.0\n");
+    try {
+        (void)mcmi::compat::parse_matrix_market<CsrMatrix, ParseError>(bad);
+        std::printf("[FAIL] ParseError not raised\n");
+        ok = false;
+    } catch (const ParseError& e) {
+        std::printf("[PASS] ParseError: %s\n", e.what());
+    }
+    return ok;
+}
+
+int main(int argc, char** argv) {
+    bool ok = io_checks();
+    if (argc > 1 && std::strcmp(argv[1], "--io-only") == 0) return ok ? 0 : 1;
     McConfig defaults;
     ok &= run("poisson2d_100", make_convection_diffusion(100, 0.0, 0.0), defaults);
     McConfig acc6;  // acceptance.cpp:257-273 criterion 6 configuration

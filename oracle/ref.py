@@ -71,6 +71,12 @@ def lib():
         L.ref_gen.restype = C.c_void_p
         L.ref_write_mm.argtypes = [C.c_int64, _i64p, _i64p, _f64p, C.c_char_p, C.c_char_p, C.c_size_t]
         L.ref_read_mm.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+        L.ref_parse_mm.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+        L.ref_format_mm.argtypes = [C.c_int64, _i64p, _i64p, _f64p, C.POINTER(C.c_size_t)]
+        L.ref_format_mm.restype = C.c_void_p
+        L.ref_free_buf.argtypes = [C.c_void_p]
+        L.ref_from_triplets.argtypes = [C.c_int64, _i64p, _i64p, _f64p, C.c_int64, C.POINTER(C.c_void_p),
+                                        C.c_char_p, C.c_size_t]
         L.ref_drop.argtypes = [C.c_int64, _i64p, _i64p, _f64p, C.c_double, C.c_int,
                                C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
         L.ref_split.argtypes = [C.c_int64, _i64p, _i64p, _f64p, C.c_double, C.c_int,
@@ -235,6 +241,45 @@ def read_mm(path: str) -> Csr:
     h = C.c_void_p()
     err = C.create_string_buffer(512)
     _check(L.ref_read_mm(path.encode(), C.byref(h), err, 512), err)
+    try:
+        return _csr_from_handle(h)
+    finally:
+        L.ref_csr_free(h)
+
+
+def parse_mm(text: bytes) -> Csr:
+    """parse_matrix_market (matrix_market.cpp:27-147) over an in-memory text."""
+    L = lib()
+    h = C.c_void_p()
+    err = C.create_string_buffer(512)
+    _check(L.ref_parse_mm(text, len(text), C.byref(h), err, 512), err)
+    try:
+        return _csr_from_handle(h)
+    finally:
+        L.ref_csr_free(h)
+
+
+def format_mm(m: Csr) -> bytes:
+    """write_matrix_market (matrix_market.cpp:155-169) into memory."""
+    L = lib()
+    rp, ci, v = m.args()
+    n = C.c_size_t()
+    p = L.ref_format_mm(m.n, _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p), C.byref(n))
+    try:
+        return C.string_at(p, n.value)
+    finally:
+        L.ref_free_buf(p)
+
+
+def from_triplets(n: int, rows, cols, vals) -> Csr:
+    """CsrMatrix::from_triplets (csr.cpp:17-58)."""
+    L = lib()
+    r = np.ascontiguousarray(rows, np.int64)
+    c = np.ascontiguousarray(cols, np.int64)
+    v = np.ascontiguousarray(vals, np.float64)
+    h = C.c_void_p()
+    err = C.create_string_buffer(512)
+    _check(L.ref_from_triplets(n, _p(r, _i64p), _p(c, _i64p), _p(v, _f64p), r.size, C.byref(h), err, 512), err)
     try:
         return _csr_from_handle(h)
     finally:

@@ -23,6 +23,7 @@
 // 3 out_of_range, 4 other.
 #include <cstdint>
 #include <cstring>
+#include <sstream>
 #include <exception>
 #include <memory>
 #include <stdexcept>
@@ -213,6 +214,44 @@ int ref_read_mm(const char* path, void** out, char* err, size_t errlen) {
     return guarded(
         [&] { *out = new CsrMatrix(read_matrix_market_file(path)); }, err,
         errlen);
+}
+
+// parse_matrix_market over an in-memory text (std::istringstream, as the
+// reference's own tests do)
+int ref_parse_mm(const char* text, size_t len, void** out, char* err, size_t errlen) {
+    *out = nullptr;
+    return guarded(
+        [&] {
+            std::istringstream in(std::string(text, len));
+            *out = new CsrMatrix(parse_matrix_market(in));
+        },
+        err, errlen);
+}
+
+// write_matrix_market into a std::ostringstream; returns a malloc'd buffer
+char* ref_format_mm(int64_t n, const int64_t* rp, const int64_t* ci, const double* v, size_t* len) {
+    std::ostringstream out;
+    write_matrix_market(to_csr(n, rp, ci, v), out);
+    const std::string s = out.str();
+    char* buf = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(buf, s.data(), s.size());
+    buf[s.size()] = 0;
+    *len = s.size();
+    return buf;
+}
+
+void ref_free_buf(char* p) { std::free(p); }
+
+int ref_from_triplets(int64_t n, const int64_t* r, const int64_t* c, const double* v, int64_t m,
+                      void** out, char* err, size_t errlen) {
+    *out = nullptr;
+    return guarded(
+        [&] {
+            *out = new CsrMatrix(CsrMatrix::from_triplets(
+                n, std::vector<index_t>(r, r + m), std::vector<index_t>(c, c + m),
+                std::vector<double>(v, v + m)));
+        },
+        err, errlen);
 }
 
 int ref_drop(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,

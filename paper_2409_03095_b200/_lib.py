@@ -13,14 +13,16 @@ from .build import LIB
 _i64p = C.POINTER(C.c_int64)
 _f64p = C.POINTER(C.c_double)
 
-MCMI_OK, MCMI_EINVAL, MCMI_ESPLIT, MCMI_ERANGE, MCMI_ECUDA, MCMI_ENOMEM, MCMI_ENODEV = range(7)
+(MCMI_OK, MCMI_EINVAL, MCMI_ESPLIT, MCMI_ERANGE, MCMI_ECUDA, MCMI_ENOMEM, MCMI_ENODEV, MCMI_EPARSE,
+ MCMI_EIO) = range(9)
 
 #: every symbol include/mcmi.h declares
 EXPORTS = [
     "mcmi_config_default", "mcmi_build", "mcmi_build_rows", "mcmi_build_into", "mcmi_result_sizes", "mcmi_result_copy",
     "mcmi_result_stats", "mcmi_result_free", "mcmi_engine_create", "mcmi_engine_destroy",
     "mcmi_engine_build", "mcmi_copy", "mcmi_version", "mcmi_solver_config_default", "mcmi_solve_device",
-    "mcmi_host_register", "mcmi_host_unregister",
+    "mcmi_host_register", "mcmi_host_unregister", "mcmi_from_triplets", "mcmi_mm_parse", "mcmi_mm_read_file",
+    "mcmi_host_csr_get", "mcmi_host_csr_free", "mcmi_mm_format", "mcmi_mm_write_file",
 ]
 
 
@@ -142,5 +144,16 @@ def load(path: str | None = None):
     L.mcmi_solve_device.argtypes = [C.POINTER(mcmi_csr_view), C.POINTER(mcmi_csr_view), C.c_void_p, C.c_void_p,
                                     C.POINTER(mcmi_solver_config), C.c_int, C.c_void_p,
                                     C.POINTER(mcmi_solve_report), C.c_char_p, C.c_size_t]
+    L.mcmi_from_triplets.argtypes = [C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                     C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+    L.mcmi_mm_parse.argtypes = [C.c_char_p, C.c_size_t, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+    L.mcmi_mm_read_file.argtypes = [C.c_char_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+    L.mcmi_host_csr_get.argtypes = [C.c_void_p, C.POINTER(mcmi_csr_view)]
+    L.mcmi_host_csr_get.restype = None
+    L.mcmi_host_csr_free.argtypes = [C.c_void_p]
+    L.mcmi_host_csr_free.restype = None
+    L.mcmi_mm_format.argtypes = [C.POINTER(mcmi_csr_view), C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t),
+                                 C.c_char_p, C.c_size_t]
+    L.mcmi_mm_write_file.argtypes = [C.POINTER(mcmi_csr_view), C.c_char_p, C.c_char_p, C.c_size_t]
     _lib = L
     return L

@@ -15,13 +15,13 @@ REPO = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIB_DIR, "libmcmi.so")
-SOURCES = ["engine.cu", "tables.cu", "walk.cu", "assemble.cu", "solver.cu"]
+SOURCES = ["engine.cu", "tables.cu", "walk.cu", "assemble.cu", "solver.cu", "mmio.cpp"]
 HEADERS = ["common.cuh", "kernels.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-fmad=false", "-std=c++17",
-    "-Xcompiler", "-fPIC,-O2", "-shared",
+    "-Xcompiler", "-fPIC,-O2,-pthread", "-shared",
     "-I", os.path.join(REPO, "include"),
 ]
 

@@ -55,6 +55,10 @@ class SplitError(RuntimeError):
     """mcspai::SplitError (split.hpp:14-16)."""
 
 
+class ParseError(RuntimeError):  # matrix_market.hpp:12-14
+    pass
+
+
 class DeviceError(RuntimeError):
     """CUDA runtime / device failure (no CPU fallback exists)."""
 
@@ -141,36 +145,41 @@ class CsrMatrix:  # csr.hpp:16-40
 
     @staticmethod
     def from_triplets(n, rows, cols, vals) -> "CsrMatrix":
-        """csr.cpp:17-58: sort by (row, col), sum duplicates, prune exact zeros."""
-        rows = np.asarray(rows, np.int64)
-        cols = np.asarray(cols, np.int64)
-        vals = np.asarray(vals, np.float64)
+        """csr.cpp:17-58 (native, mcmi_from_triplets): sort by (row, col), sum
+        duplicates in the reference's sort order, prune exact zeros."""
+        rows = np.ascontiguousarray(rows, np.int64)
+        cols = np.ascontiguousarray(cols, np.int64)
+        vals = np.ascontiguousarray(vals, np.float64)
         if not (rows.size == cols.size == vals.size):
             raise ValueError("triplet arrays must have equal length")
-        if rows.size and (rows.min() < 0 or rows.max() >= n or cols.min() < 0 or cols.max() >= n):
-            raise IndexError("triplet index out of range")
-        order = np.lexsort((cols, rows))  # stable
-        r, c, v = rows[order], cols[order], vals[order]
-        if r.size:
-            new = np.ones(r.size, bool)
-            new[1:] = (r[1:] != r[:-1]) | (c[1:] != c[:-1])
-            starts = np.flatnonzero(new)
-            # duplicates are summed in stored order (left fold)
-            sums = np.array([_fold(v[s:e]) for s, e in zip(starts, list(starts[1:]) + [r.size])]) \
-                if (~new).any() else v[starts]
-            r, c, v = r[starts], c[starts], sums
-            keep = v != 0.0
-            r, c, v = r[keep], c[keep], v[keep]
-        rp = np.zeros(n + 1, np.int64)
-        np.add.at(rp, r + 1, 1)
-        return CsrMatrix(n, np.cumsum(rp), c, v)
+        h = C.c_void_p()
+        err = C.create_string_buffer(512)
+        code = L.load().mcmi_from_triplets(int(n), rows.ctypes.data, cols.ctypes.data, vals.ctypes.data,
+                                           rows.size, C.byref(h), err, 512)
+        raise_for(code, err.value.decode(errors="replace"))
+        return host_csr_take(h)
 
 
-def _fold(x):
-    s = 0.0
-    for t in x:
-        s += float(t)
-    return s
+def host_csr_take(h) -> CsrMatrix:
+    """Copies a library-owned mcmi_host_csr into a CsrMatrix and frees it."""
+    lib = L.load()
+    try:
+        v = L.mcmi_csr_view()
+        lib.mcmi_host_csr_get(h, C.byref(v))
+        n = int(v.n)
+        nnz = 0
+        rp = np.zeros(max(n, 0) + 1, np.int64)
+        if n > 0:
+            C.memmove(rp.ctypes.data, v.row_ptr, (n + 1) * 8)
+            nnz = int(rp[-1])
+        ci = np.empty(nnz, np.int64)
+        vals = np.empty(nnz, np.float64)
+        if nnz:
+            C.memmove(ci.ctypes.data, v.col_idx, nnz * 8)
+            C.memmove(vals.ctypes.data, v.values, nnz * 8)
+        return CsrMatrix(n, rp, ci, vals)
+    finally:
+        lib.mcmi_host_csr_free(h)
 
 
 @dataclass
@@ -206,6 +215,10 @@ def raise_for(code: int, msg: str):
         raise IndexError(msg)
     if code == L.MCMI_ENOMEM:
         raise MemoryError(msg)
+    if code == L.MCMI_EPARSE:
+        raise ParseError(msg)
+    if code == L.MCMI_EIO:
+        raise RuntimeError(msg)
     raise DeviceError(f"[status {code}] {msg}")
 
 

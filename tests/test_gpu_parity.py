@@ -357,9 +357,8 @@ def test_streamed_build_into_equals_handle_path(mc, rng):
             assert np.array_equal(got.row_meta.entries_before_retention, want.row_meta.entries_before_retention)
         lo, hi = b.n // 3, b.n - 5
         part = mc.compute_preconditioner(b, cfg, rows=(lo, hi))
-        out = {"row_ptr": np.empty(hi - lo + 1, np.int64), "col_idx": np.empty(part.m.nnz()),
+        out = {"row_ptr": np.empty(hi - lo + 1, np.int64), "col_idx": np.empty(part.m.nnz(), np.int64),
                "values": np.empty(part.m.nnz())}
-        out["col_idx"] = out["col_idx"].astype(np.int64)
         got = mc.compute_preconditioner(b, cfg, out=out, rows=(lo, hi))
         assert got.m == part.m
 

@@ -1,0 +1,292 @@
+"""Matrix Market I/O and from_triplets (§8f rank 2) against the reference.
+
+The checker is the unmodified reference library (oracle/_ref, built from
+/root/reference/proj/src by oracle/Makefile): its parse_matrix_market over an
+std::istringstream, its write_matrix_market into an std::ostringstream and its
+CsrMatrix::from_triplets.  Parity is byte-exact: identical CSR arrays (value
+bits included), identical output text, identical error class and message.
+CPU only: the I/O path runs on the host.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from helpers import bits_equal
+
+ref = pytest.importorskip("oracle.ref")
+if not ref.available():
+    pytest.skip("oracle/_ref not built", allow_module_level=True)
+
+from paper_2409_03095_b200 import CsrMatrix  # noqa: E402
+from paper_2409_03095_b200 import matrix_market as mm  # noqa: E402
+from paper_2409_03095_b200.mcspai import ParseError  # noqa: E402
+
+
+def same(a: CsrMatrix, r) -> bool:
+    return (a.n == r.n and np.array_equal(a.row_ptr, r.row_ptr) and np.array_equal(a.col_idx, r.col_idx)
+            and bits_equal(a.values, r.values))
+
+
+def run_both(text: bytes):
+    """(ours, reference): each a CsrMatrix/Csr, ('error', message) for a
+    ParseError or ('other', message) for any other exception."""
+    try:
+        got = mm.parse_matrix_market(text)
+    except ParseError as e:
+        got = ("error", str(e))
+    except (ValueError, IndexError) as e:
+        got = ("other", str(e))
+    try:
+        want = ref.parse_mm(text)
+    except ref.RefError as e:
+        parse_error = e.code == 4 and str(e).startswith("matrix market:")
+        want = ("error" if parse_error else "other", str(e))
+    return got, want
+
+
+def check_text(text: bytes):
+    got, want = run_both(text)
+    # Documented deviation: a negative dimension makes the reference throw
+    # std::length_error from std::vector (n < -1) or return an n = -1 matrix
+    # without row_ptr; the library refuses it with "negative dimension".
+    if (isinstance(want, tuple) and "max_size" in want[1]) or (not isinstance(want, tuple) and want.n < 0):
+        assert got == ("other", "negative dimension"), (text[:300], got)
+        return
+    if isinstance(want, tuple):
+        assert got == want, (text[:300], got, want)
+    else:
+        assert not isinstance(got, tuple), (text[:300], got)
+        assert same(got, want), text[:300]
+
+
+# ------------------------------------------------ the reference's own cases
+REF_CASES = [  # test_sparse_core.cpp:50-117
+    b"%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 1.0\n2 2 1.0\n",
+    b"%%MatrixMarket matrix coordinate real general\n2 2 2\n1 1 2.0\n1 1 3.0\n",
+    b"%%MatrixMarket matrix coordinate real symmetric\n% comment line\n3 3 3\n1 1 4.0\n2 1 -1.0\n3 3 2.0\n",
+    b"%%MatrixMarket matrix array real general\n2 2\n1.5\n0.0\n-2.0\n4.0\n",
+    b"%%NotMM matrix coordinate real general\n",
+    b"%%MatrixMarket matrix coordinate real general\n2 3 1\n1 1 1.0\n",
+    b"%%MatrixMarket matrix coordinate complex general\n1 1 1\n1 1 1.0 0.0\n",
+]
+
+
+@pytest.mark.parametrize("text", REF_CASES)
+def test_reference_cases(text):
+    check_text(text)
+
+
+# num_get token boundaries: where one extraction stops the next one starts
+TOKEN_CASES = [b"0e5 1.0 2 3", b"1.5-2.0 3 4", b"5.e3 .5 -.5 +1", b"1e5.5 2 3", b"1e+5e3 2 3",
+               b"00.5 1 2 3", b"1e 2 3 4", b"1.2.3 4 5", b"7\t8\r9 10", b"-0 +0 0. .0", b"0x10 1 2 3"]
+
+
+@pytest.mark.parametrize("line", TOKEN_CASES)
+def test_array_token_boundaries(line):
+    check_text(b"%%MatrixMarket matrix array real general\n2 2\n" + line + b"\n1 2 3 4\n")
+    check_text(b"%%MatrixMarket matrix coordinate real general\n4 4 1\n" + line + b"\n")
+
+
+def test_reference_case_values():
+    m = mm.parse_matrix_market(REF_CASES[1])
+    assert m.nnz() == 1 and m.at(0, 0) == 5.0
+    m = mm.parse_matrix_market(REF_CASES[3])
+    assert m.nnz() == 3 and m.at(0, 1) == -2.0 and m.at(1, 0) == 0.0
+    with pytest.raises(ParseError, match="line 2"):
+        mm.parse_matrix_market(REF_CASES[5])
+
+
+def test_roundtrip_reference_values():  # test_sparse_core.cpp:119-135
+    for m in [CsrMatrix.identity(2), CsrMatrix.from_triplets(3, [0, 2], [1, 0], [0.25, -1e-17]),
+              CsrMatrix.from_triplets(2, [0, 1], [0, 1], [1.0 / 3.0, 4.9406564584124654e-324])]:
+        assert mm.parse_matrix_market(mm.format_matrix_market(m)) == m
+
+
+# --------------------------------------------------------------- writing
+def random_csr(rng, n, fill, special=False) -> CsrMatrix:
+    rows, cols = np.nonzero(rng.random((n, n)) < fill)
+    vals = rng.standard_normal(rows.size) * 10.0 ** rng.integers(-300, 300, rows.size)
+    if special and vals.size:
+        pick = rng.integers(0, vals.size, max(1, vals.size // 10))
+        vals[pick] = rng.choice([4.9406564584124654e-324, -2.2250738585072014e-308, 1.7976931348623157e308,
+                                 -0.0, 1e16, 123456789012345678.0, 0.1, 1.0 / 3.0], pick.size)
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, rows + 1, 1)
+    return CsrMatrix(n, np.cumsum(rp), cols.astype(np.int64), vals)
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_format_bytes_match(seed):
+    rng = np.random.default_rng(seed)
+    m = random_csr(rng, int(rng.integers(0, 60)), 0.2, special=True)
+    assert mm.format_matrix_market(m) == ref.format_mm(ref.Csr(m.n, m.row_ptr, m.col_idx, m.values))
+
+
+def test_format_large_parallel():
+    rng = np.random.default_rng(5)
+    m = random_csr(rng, 1500, 0.2)  # ~450k entries: several formatting threads
+    text = mm.format_matrix_market(m)
+    assert text == ref.format_mm(ref.Csr(m.n, m.row_ptr, m.col_idx, m.values))
+    assert mm.parse_matrix_market(text) == m
+
+
+def test_files(tmp_path):
+    rng = np.random.default_rng(9)
+    m = random_csr(rng, 200, 0.05)
+    ours, theirs = tmp_path / "ours.mtx", tmp_path / "ref.mtx"
+    mm.write_matrix_market_file(m, ours)
+    ref.write_mm(ref.Csr(m.n, m.row_ptr, m.col_idx, m.values), str(theirs))
+    assert ours.read_bytes() == theirs.read_bytes()
+    assert mm.read_matrix_market_file(theirs) == m
+    with pytest.raises(ParseError, match="cannot open"):
+        mm.read_matrix_market_file(tmp_path / "missing.mtx")
+    with pytest.raises(RuntimeError, match="cannot open"):
+        mm.write_matrix_market_file(m, tmp_path / "no_such_dir" / "x.mtx")
+    assert mm.write_matrix_market(m) == ours.read_text()
+
+
+# --------------------------------------------------------------- parsing
+NUM_TOKENS = ["1", "+1", "-0", "01", "1.5", "-.5", "5.", "1e5", "1E-5", "0e5", "00.5", "1e", "1e+", "1ex",
+              ".", "-", "+", "inf", "nan", "0x10", "1.5.2", "1e5.5", "3-4", "1e400", "-1e400", "1e-400",
+              "4.9406564584124654e-324", "2.5e-3", "7", "-3", "12345678901234567890", "9223372036854775807",
+              "-9223372036854775808", "+-1", ".e5", "5.e3", "1e+5e3", "2", "3", "0", "-1.25E+2"]
+
+
+def rand_entry_line(rng, n):
+    kind = rng.random()
+    if kind < 0.7:
+        i, j = rng.integers(1, n + 1, 2) if n > 0 else (1, 1)
+        v = rng.choice(["1.5", "-2", "0.25", "3e-2", "0", "-0.0", "1e300", "7.125"])
+        sep = rng.choice([" ", "  ", "\t", " \t "])
+        return f"{i}{sep}{j}{sep}{v}"
+    if kind < 0.8:
+        return " ".join(rng.choice(NUM_TOKENS, int(rng.integers(1, 5))))
+    if kind < 0.88:
+        return "% comment " + str(rng.integers(0, 99))
+    if kind < 0.94:
+        return rng.choice(["", " ", "\t", "\r"])
+    i, j = rng.integers(-1, n + 3, 2)
+    return f"{i} {j} 1.0"
+
+
+def rand_text(rng) -> bytes:
+    n = int(rng.integers(0, 7))
+    fmt = rng.choice(["coordinate", "array", "Coordinate", "ARRAY", "dense"])
+    field = rng.choice(["real", "real", "integer", "double", "pattern", "complex", "Real", "weird"])
+    sym = rng.choice(["general", "general", "symmetric", "skew-symmetric", "Symmetric", "hermitian", ""])
+    banner = rng.choice(["%%MatrixMarket", "%%MatrixMarket", "%%MatrixMarket", "%MatrixMarket", ""])
+    lines = [f"{banner} {rng.choice(['matrix', 'matrix', 'Matrix', 'vector'])} {fmt} {field} {sym}"]
+    for _ in range(int(rng.integers(0, 3))):
+        lines.append(rng.choice(["% c", "", "%%"]))
+    if rng.random() < 0.9:
+        if "oord" in fmt.lower() or rng.random() < 0.3:
+            declared = int(rng.integers(0, 8))
+            size = rng.choice([f"{n} {n} {declared}", f"{n} {n + 1} {declared}", f"{n} {n}", f"{n}",
+                               f"{n} {n} {declared} extra", f"{n}.0 {n} {declared}", f"-{n} -{n} 0",
+                               f"{n} {n} -1"], p=[.7, .05, .05, .04, .04, .04, .04, .04])
+        else:
+            size = rng.choice([f"{n} {n}", f"{n} {n + 1}", f"{n}"], p=[.9, .05, .05])
+        lines.append(size)
+        for _ in range(int(rng.integers(0, 12))):
+            if "rray" in fmt.lower() and rng.random() < 0.7:
+                lines.append(" ".join(rng.choice(NUM_TOKENS, int(rng.integers(1, 4)))))
+            else:
+                lines.append(rand_entry_line(rng, n))
+    text = "\n".join(lines)
+    if rng.random() < 0.7:
+        text += "\n"
+    if rng.random() < 0.1:
+        text = text.replace("\n", "\r\n")
+    return text.encode()
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_parse_fuzz(seed):
+    rng = np.random.default_rng(1000 + seed)
+    for _ in range(1500):
+        check_text(rand_text(rng))
+
+
+@pytest.mark.parametrize("sym", ["general", "symmetric", "skew-symmetric"])
+def test_parse_large_chunked(sym):
+    """Several MB of entries: the parallel chunked parse, with the declared
+    count cutting the file short, duplicates, comments and a bad line past the
+    declared count (ignored, as in the reference)."""
+    rng = np.random.default_rng(7)
+    n, m = 5000, 400_000
+    i = rng.integers(1, n + 1, m)
+    j = rng.integers(1, n + 1, m)
+    v = rng.standard_normal(m)
+    body = [f"{a} {b} {c!r}" for a, b, c in zip(i, j, v)]
+    for k in rng.integers(0, m, 50):
+        body[k] = "% interleaved comment"
+    declared = m - 1000
+    tail = ["1 1 not-a-number", "99999999 1 1.0"]
+    text = "\n".join([f"%%MatrixMarket matrix coordinate real {sym}", f"{n} {n} {declared}"] + body + tail) + "\n"
+    check_text(text.encode())
+    # an error inside the declared range, in a late chunk
+    bad = list(body)
+    bad[int(m * 0.8)] = "3 x 1.0"
+    check_text("\n".join([f"%%MatrixMarket matrix coordinate real {sym}", f"{n} {n} {declared}"] + bad).encode())
+    # too few entries: end of file
+    check_text("\n".join([f"%%MatrixMarket matrix coordinate real {sym}", f"{n} {n} {m + 5}"] + body).encode())
+
+
+# ---------------------------------------------------------- from_triplets
+@pytest.mark.parametrize("seed,n,m,span", [(0, 5, 40, 3), (1, 50, 3000, 20), (2, 300, 200_000, 40),
+                                           (3, 1, 1000, 1), (4, 100, 50_000, 100), (5, 7, 0, 1)])
+def test_from_triplets_duplicates(seed, n, m, span):
+    """Coordinates repeated 3+ times: summed in libstdc++ std::sort's tie order."""
+    rng = np.random.default_rng(seed)
+    r = rng.integers(0, n, m)
+    c = rng.integers(0, min(n, span), m)
+    v = rng.standard_normal(m) * 10.0 ** rng.integers(-8, 8, m)
+    got = CsrMatrix.from_triplets(n, r, c, v)
+    assert same(got, ref.from_triplets(n, r, c, v))
+
+
+def test_from_triplets_pairs_parallel():
+    """Every coordinate at most twice (the parallel path) at a size that uses
+    all threads, including exact cancellations."""
+    rng = np.random.default_rng(11)
+    n, m = 20000, 600_000
+    r = rng.integers(0, n, m)
+    c = rng.integers(0, n, m)
+    key = np.unique(r * n + c)
+    r, c = key // n, key % n
+    v = rng.standard_normal(r.size)
+    dup = rng.random(r.size) < 0.3
+    r2, c2 = r[dup], c[dup]
+    v2 = np.where(rng.random(dup.sum()) < 0.2, -v[dup], rng.standard_normal(dup.sum()))
+    rr, cc, vv = np.concatenate([r, r2]), np.concatenate([c, c2]), np.concatenate([v, v2])
+    perm = rng.permutation(rr.size)
+    rr, cc, vv = rr[perm], cc[perm], vv[perm]
+    assert same(CsrMatrix.from_triplets(n, rr, cc, vv), ref.from_triplets(n, rr, cc, vv))
+
+
+def test_from_triplets_errors():
+    with pytest.raises(IndexError, match="triplet index out of range"):
+        CsrMatrix.from_triplets(3, [0, 3], [0, 0], [1.0, 1.0])
+    with pytest.raises(ValueError, match="equal length"):
+        CsrMatrix.from_triplets(3, [0, 1], [0], [1.0, 1.0])
+    with pytest.raises(ref.RefError):
+        ref.from_triplets(3, [0, -1], [0, 0], [1.0, 1.0])
+    z = CsrMatrix.from_triplets(2, [0, 0], [1, 1], [2.0, -2.0])  # exact cancellation pruned
+    assert z.nnz() == 0
+
+
+def test_io_threads_env_is_harmless():
+    assert int(os.environ.get("MCMI_IO_THREADS", "1")) >= 1
+
+
+def test_cpp_dropin_io():
+    """include/mcmi/mcspai_compat.hpp's Matrix Market / from_triplets templates
+    on the reference's own types (oracle/dropin_demo.cpp --io-only)."""
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "dropin_demo")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/dropin_demo not built")
+    r = subprocess.run([exe, "--io-only"], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "FAIL" not in r.stdout
