@@ -82,6 +82,10 @@ struct WalkArgs {
     int log_stride;         // max(max_len, 1) step deposits per chain
     unsigned log_magic;     // ceil(2^32 / log_stride) for log_stride >= 2: p / S == __umulhi(p, magic)
     int ell0;               // initial speculative draw stride (reference-stream mode)
+    int log_n;              // launch_walk: round32(lanes * log_stride), deposit-log slots per warp
+    int hash_shift;         // launch_walk: 32 - log2(cap)
+    int log_shift;          // launch_walk: log2(log_stride) if a power of two, else -1
+    long long warp_bytes;   // launch_walk: shared/global bytes per warp
     int deg_stats;          // count sum deg(s) (MCMI_FLAG_DEG_STATS)
     unsigned char* gscratch;  // global-tier per-warp accumulator + log (nullptr for smem tiers)
     // outputs, indexed by local row (row - row_begin)

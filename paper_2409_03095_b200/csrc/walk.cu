@@ -386,16 +386,16 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     const int cap = a.cap;
     const int S = a.log_stride;                 // step deposits per chain (max_len)
     const int B = a.lanes;                      // chains per batch
-    const int logn = round32(B * S);
-    const size_t per_warp = static_cast<size_t>(cap + logn) * 12;
+    const int logn = a.log_n;                   // round32(B * S), host-computed (kernel parameter)
+    const size_t per_warp = static_cast<size_t>(a.warp_bytes);
     // GL: per-warp accumulator + log in global scratch (large rows / long walks)
     unsigned char* wbase = GL ? a.gscratch + per_warp * (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp)
                               : smem_raw + per_warp * warp;
     const WarpSmem sm = carve(wbase, cap, logn);
     const unsigned cap_mask = static_cast<unsigned>(cap - 1);
-    const int shift = 32 - (31 - __clz(cap));
+    const int shift = a.hash_shift;             // 32 - log2(cap)
     const unsigned lt_mask = (1u << lane) - 1u;
-    const int s_shift = (S & (S - 1)) == 0 ? 31 - __clz(S) : -1;  // log2(S) when S is a power of two
+    const int s_shift = a.log_shift;            // log2(S) when S is a power of two, else -1
 
     const uint4* __restrict__ rec = a.t.rec;
     const double2* __restrict__ ent = a.t.ent;
@@ -905,9 +905,24 @@ int walk_minb() {
     return v;
 }
 
-cudaError_t launch_walk(const WalkArgs& a, int warps_per_block, int num_sms, bool global_tier,
+cudaError_t launch_walk(const WalkArgs& a_in, int warps_per_block, int num_sms, bool global_tier,
                         int64_t max_warps, cudaStream_t s) {
-    if (a.n_work <= 0) return cudaSuccess;
+    if (a_in.n_work <= 0) return cudaSuccess;
+    WalkArgs a = a_in;  // derived per-launch constants, so the kernel re-reads rather than recomputes them
+    a.log_n = round32(a.lanes * a.log_stride);
+    a.warp_bytes = static_cast<long long>(walk_smem_bytes_per_warp(a.cap, a.lanes, a.log_stride));
+    {
+        int lg = 0;
+        while ((1 << lg) < a.cap) ++lg;
+        a.hash_shift = 32 - lg;
+        const int S = a.log_stride;
+        int ls = -1;
+        if ((S & (S - 1)) == 0) {
+            ls = 0;
+            while ((1 << ls) < S) ++ls;
+        }
+        a.log_shift = ls;
+    }
     const int mb = walk_minb();
     const bool pos64 = static_cast<double>(a.n_chains) * static_cast<double>(std::max<int64_t>(a.max_len, 1)) >=
                            4294967295.0 ||  // draw positions beyond 32 bits
