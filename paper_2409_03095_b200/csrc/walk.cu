@@ -343,8 +343,46 @@ __device__ void warp_bitonic(int* keys, double* vals, int P) {
     }
 }
 
-// Sorts (keys, vals)[0, s) by column: register rank sort for s <= 32, bitonic
-// otherwise (pads [s, P) with INT_MAX); returns the padded length touched.
+// Rank sort of (keys, vals)[0, s), s <= 32*E, distinct keys: lane l holds
+// entries l, l+32, ...; each entry's destination is the number of smaller
+// keys, counted against a broadcast read of every key (s reads per lane, no
+// barriers), then everything is scattered at once.
+template <int E>
+__device__ __forceinline__ void warp_rank_sort(int* keys, double* vals, int s) {
+    const int lane = static_cast<int>(threadIdx.x & 31);
+    int k[E], r[E];
+    double v[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = lane + 32 * e;
+        k[e] = i < s ? keys[i] : INT_MAX;
+        v[e] = i < s ? vals[i] : 0.0;
+        r[e] = 0;
+    }
+    int j = 0;
+    for (; j + 4 <= s; j += 4) {
+        const int4 q = *reinterpret_cast<const int4*>(keys + j);
+#pragma unroll
+        for (int e = 0; e < E; ++e) r[e] += (q.x < k[e]) + (q.y < k[e]) + (q.z < k[e]) + (q.w < k[e]);
+    }
+    for (; j < s; ++j) {
+        const int q = keys[j];
+#pragma unroll
+        for (int e = 0; e < E; ++e) r[e] += q < k[e];
+    }
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; ++e)
+        if (lane + 32 * e < s) {
+            keys[r[e]] = k[e];
+            vals[r[e]] = v[e];
+        }
+    __syncwarp();
+}
+
+// Sorts (keys, vals)[0, s) by column: rank sorts for s <= 128 (register rank
+// sort for s <= 32), bitonic otherwise (pads [s, P) with INT_MAX); returns the
+// padded length touched.
 __device__ int sort_by_column(int* keys, double* vals, int s) {
     const int lane = static_cast<int>(threadIdx.x & 31);
     if (s <= 32) {
@@ -359,6 +397,14 @@ __device__ int sort_by_column(int* keys, double* vals, int s) {
             vals[pos] = vv;
         }
         __syncwarp();
+        return s;
+    }
+    if (s <= 64) {
+        warp_rank_sort<2>(keys, vals, s);
+        return s;
+    }
+    if (s <= 128) {
+        warp_rank_sort<4>(keys, vals, s);
         return s;
     }
     int P = 64;
