@@ -614,8 +614,26 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     } else {
         // ---- streamed: row chunks; chunk c's device->host copy (copy stream)
         // overlaps chunk c+1's walk (compute stream).  Double-buffered slabs.
-        const int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(16, (rows + 131071) / 131072));
-        const int64_t chunk = (rows + nchunk - 1) / nchunk;
+        // Chunk sizes fall geometrically: few chunk boundaries (each costs the
+        // walk kernel's tail) and a small last chunk (its copy is the exposed
+        // one).  MCMI_STREAM_CHUNKS / MCMI_STREAM_RATIO: tuning overrides.
+        int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(8, rows / 65536));
+        double ratio = 0.65;
+        if (const char* v = getenv("MCMI_STREAM_CHUNKS")) nchunk = std::max<int64_t>(1, std::min<int64_t>(64, atoll(v)));
+        if (const char* v = getenv("MCMI_STREAM_RATIO")) ratio = std::max(0.05, std::min(1.0, atof(v)));
+        nchunk = std::min<int64_t>(nchunk, std::max<int64_t>(rows, 1));
+        std::vector<int64_t> bound(nchunk + 1, 0);
+        {
+            double wsum = 0.0, w = 1.0;
+            for (int64_t c = 0; c < nchunk; ++c, w *= ratio) wsum += w;
+            double acc = 0.0;
+            w = 1.0;
+            for (int64_t c = 1; c < nchunk; ++c, w *= ratio) {
+                acc += w;
+                bound[c] = std::max(bound[c - 1] + 1, static_cast<int64_t>(static_cast<double>(rows) * acc / wsum));
+            }
+            bound[nchunk] = rows;
+        }
         MCMI_TRY(e->ensure_copy_stream(), "copy stream");
         MCMI_TRY(cudaStreamSynchronize(e->copy), "drain copies");
         // row pointers of all chunks accumulate in out_rp; only col/val stream per chunk
@@ -632,8 +650,8 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         for (auto& ev : dev) cudaEventCreate(&ev);
         for (int64_t c = 0; c < nchunk; ++c) {
             if (dbg) cudaEventRecord(dev[4 * c], s);
-            const int64_t lo = c * chunk, hi = std::min(rows, lo + chunk);
-            if (lo >= hi) break;
+            const int64_t lo = bound[c], hi = std::min(rows, bound[c + 1]);
+            if (lo >= hi) continue;
             if (c > 0) pool_used = 0;  // staging reused per chunk (chunk 0 keeps the pilot rows' slots)
             Status ws = walk_rows(c == 0 ? pilot_rows : lo, hi);
             if (ws.code) return ws;
