@@ -45,6 +45,7 @@ extern "C" {
 #define MCMI_ENODEV 6  /* no CUDA device / device ordinal invalid */
 #define MCMI_EPARSE 7  /* mcspai::ParseError (matrix_market.hpp:12-14), message names the line */
 #define MCMI_EIO 8     /* std::runtime_error from file I/O (cannot open / write failure) */
+#define MCMI_ERECOVERY 9 /* mcspai::RecoveryError (recovery.hpp:9-11): "singular update at row i" */
 
 /* AugmentationMode (split.hpp:9-12) */
 #define MCMI_AUGMENT_PLAIN 0
@@ -241,6 +242,21 @@ void mcmi_host_csr_free(mcmi_host_csr* m);
 int mcmi_mm_format(const mcmi_csr_view* m, char* buf, size_t cap, size_t* len, char* err, size_t errlen);
 /* mcspai::write_matrix_market_file (matrix_market.cpp:171-177) */
 int mcmi_mm_write_file(const mcmi_csr_view* m, const char* path, char* err, size_t errlen);
+
+/* ------------------------------------------------ recovery phase (§8f rank 4) */
+
+/* mcspai::recover_inverse (recovery.hpp:22-23, recovery.cpp:7-33) on the GPU:
+ * m is the dense row-major n x n B_hat^{-1} (host memory) and is replaced by
+ * the recovered inverse, bit-identical to the reference.  s_diag / s_len are
+ * RecoveryPlan::s_diag.  Errors: MCMI_EINVAL ("recovery plan length mismatch",
+ * "tol must be positive"), MCMI_ERECOVERY ("singular update at row i"; m is
+ * left unchanged). */
+int mcmi_recover_inverse(double* m, int64_t n, const double* s_diag, int64_t s_len, double tol, int device,
+                         char* err, size_t errlen);
+/* The same on a device-resident matrix, in place, on `stream` (m_dev is left
+ * partially updated on MCMI_ERECOVERY, like the reference's working copy). */
+int mcmi_recover_inverse_device(double* m_dev, int64_t n, const double* s_diag, int64_t s_len, double tol,
+                                int device, void* stream, char* err, size_t errlen);
 
 /* Library identification: returns "mcmi <abi> sm_100a". */
 const char* mcmi_version(void);

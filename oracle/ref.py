@@ -75,6 +75,8 @@ def lib():
         L.ref_format_mm.argtypes = [C.c_int64, _i64p, _i64p, _f64p, C.POINTER(C.c_size_t)]
         L.ref_format_mm.restype = C.c_void_p
         L.ref_free_buf.argtypes = [C.c_void_p]
+        L.ref_recover.argtypes = [C.c_int64, _f64p, _f64p, C.c_int64, C.c_double, _f64p, C.c_char_p, C.c_size_t]
+        L.ref_dense_inverse.argtypes = [C.c_int64, _f64p, _f64p, C.c_char_p, C.c_size_t]
         L.ref_from_triplets.argtypes = [C.c_int64, _i64p, _i64p, _f64p, C.c_int64, C.POINTER(C.c_void_p),
                                         C.c_char_p, C.c_size_t]
         L.ref_drop.argtypes = [C.c_int64, _i64p, _i64p, _f64p, C.c_double, C.c_int,
@@ -269,6 +271,27 @@ def format_mm(m: Csr) -> bytes:
         return C.string_at(p, n.value)
     finally:
         L.ref_free_buf(p)
+
+
+def recover_inverse(m, s_diag, tol: float = 1e-12):
+    """recover_inverse (recovery.cpp:7-33) on a dense row-major n x n matrix."""
+    L = lib()
+    a = np.ascontiguousarray(m, np.float64)
+    s = np.ascontiguousarray(s_diag, np.float64)
+    out = np.empty_like(a)
+    err = C.create_string_buffer(512)
+    _check(L.ref_recover(a.shape[0], _p(a, _f64p), _p(s, _f64p), s.size, tol, _p(out, _f64p), err, 512), err)
+    return out
+
+
+def dense_inverse(m):
+    """dense_inverse (dense_solve.cpp): Gauss-Jordan with partial pivoting."""
+    L = lib()
+    a = np.ascontiguousarray(m, np.float64)
+    out = np.empty_like(a)
+    err = C.create_string_buffer(512)
+    _check(L.ref_dense_inverse(a.shape[0], _p(a, _f64p), _p(out, _f64p), err, 512), err)
+    return out
 
 
 def from_triplets(n: int, rows, cols, vals) -> Csr:

@@ -30,7 +30,9 @@
 #include <string>
 
 #include "mcspai/csr.hpp"
+#include "mcspai/dense_solve.hpp"
 #include "mcspai/matrix_market.hpp"
+#include "mcspai/recovery.hpp"
 #include "mcspai/mc_engine.hpp"
 #include "mcspai/solvers.hpp"
 #include "mcspai/split.hpp"
@@ -241,6 +243,36 @@ char* ref_format_mm(int64_t n, const int64_t* rp, const int64_t* ci, const doubl
 }
 
 void ref_free_buf(char* p) { std::free(p); }
+
+// recover_inverse (recovery.cpp:7-33): out = recovered n x n (row-major);
+// status 5 = RecoveryError, 1 = invalid_argument
+int ref_recover(int64_t n, const double* m, const double* s, int64_t s_len, double tol, double* out,
+                char* err, size_t errlen) {
+    try {
+        DenseMatrix d(n);
+        std::memcpy(d.values.data(), m, sizeof(double) * n * n);
+        RecoveryPlan plan{std::vector<double>(s, s + s_len)};
+        const DenseMatrix r = recover_inverse(d, plan, tol);
+        std::memcpy(out, r.values.data(), sizeof(double) * n * n);
+        return 0;
+    } catch (const RecoveryError& e) {
+        return fail(e, 5, err, errlen);
+    } catch (const std::invalid_argument& e) {
+        return fail(e, 1, err, errlen);
+    }
+}
+
+// dense_inverse (dense_solve.cpp) — produces B_hat^{-1} inputs like the reference tests
+int ref_dense_inverse(int64_t n, const double* m, double* out, char* err, size_t errlen) {
+    return guarded(
+        [&] {
+            DenseMatrix d(n);
+            std::memcpy(d.values.data(), m, sizeof(double) * n * n);
+            const DenseMatrix r = dense_inverse(d);
+            std::memcpy(out, r.values.data(), sizeof(double) * n * n);
+        },
+        err, errlen);
+}
 
 int ref_from_triplets(int64_t n, const int64_t* r, const int64_t* c, const double* v, int64_t m,
                       void** out, char* err, size_t errlen) {

@@ -14,7 +14,7 @@ _i64p = C.POINTER(C.c_int64)
 _f64p = C.POINTER(C.c_double)
 
 (MCMI_OK, MCMI_EINVAL, MCMI_ESPLIT, MCMI_ERANGE, MCMI_ECUDA, MCMI_ENOMEM, MCMI_ENODEV, MCMI_EPARSE,
- MCMI_EIO) = range(9)
+ MCMI_EIO, MCMI_ERECOVERY) = range(10)
 
 #: every symbol include/mcmi.h declares
 EXPORTS = [
@@ -22,7 +22,8 @@ EXPORTS = [
     "mcmi_result_stats", "mcmi_result_free", "mcmi_engine_create", "mcmi_engine_destroy",
     "mcmi_engine_build", "mcmi_copy", "mcmi_version", "mcmi_solver_config_default", "mcmi_solve_device",
     "mcmi_host_register", "mcmi_host_unregister", "mcmi_from_triplets", "mcmi_mm_parse", "mcmi_mm_read_file",
-    "mcmi_host_csr_get", "mcmi_host_csr_free", "mcmi_mm_format", "mcmi_mm_write_file",
+    "mcmi_host_csr_get", "mcmi_host_csr_free", "mcmi_mm_format", "mcmi_mm_write_file", "mcmi_recover_inverse",
+    "mcmi_recover_inverse_device",
 ]
 
 
@@ -155,5 +156,9 @@ def load(path: str | None = None):
     L.mcmi_mm_format.argtypes = [C.POINTER(mcmi_csr_view), C.c_void_p, C.c_size_t, C.POINTER(C.c_size_t),
                                  C.c_char_p, C.c_size_t]
     L.mcmi_mm_write_file.argtypes = [C.POINTER(mcmi_csr_view), C.c_char_p, C.c_char_p, C.c_size_t]
+    L.mcmi_recover_inverse.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_double, C.c_int,
+                                       C.c_char_p, C.c_size_t]
+    L.mcmi_recover_inverse_device.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_double, C.c_int,
+                                              C.c_void_p, C.c_char_p, C.c_size_t]
     _lib = L
     return L

@@ -125,6 +125,12 @@ cudaError_t launch_compact(const int* stage_col, const double* stage_val, const 
                            const int* row_cnt, const int64_t* row_ptr, int64_t rows,
                            int64_t* col_out, double* val_out, cudaStream_t s);
 
+// Recovery phase (recovery.cu): in-place recover_inverse on a device n x n
+// row-major matrix; s_host = the plan's s_diag on the host.  *bad_row = the
+// row of a singular update (MCMI_ERECOVERY) or -1.
+int recover_device(double* m, int64_t n, const double* s_host, double tol, cudaStream_t st, int64_t* bad_row,
+                   std::string& msg);
+
 // Validation solvers on device (solver.cu).
 int solve_device(const mcmi_csr_view& b, const mcmi_csr_view* m, const double* rhs, double* x,
                  const mcmi_solver_config& cfg, cudaStream_t s, mcmi_solve_report* rep, std::string& msg);
