@@ -45,6 +45,8 @@ def parse():
     p.add_argument("--cpu-seconds", type=float, default=12.0, help="target CPU work of the baseline sample")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--assembly", default="p2p", choices=["p2p", "nccl"],
+                   help="multi-GPU assembly of M: fused peer stores (default) or NCCL all-gather-v")
     return p.parse_args()
 
 
@@ -233,7 +235,7 @@ def run_ours(args):
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
 
-    from paper_2409_03095_b200.distributed import allgatherv_csr, partition_rows
+    from paper_2409_03095_b200.distributed import SymmetricM, allgatherv_csr, assemble_p2p, partition_rows
     from paper_2409_03095_b200.engine import DeviceEngine
     from paper_2409_03095_b200.mcspai import McConfig, RngMode, compute_preconditioner
 
@@ -245,13 +247,41 @@ def run_ours(args):
     d_rp, d_ci, d_v = DeviceEngine.upload(b, local)
     stream = torch.cuda.current_stream(device)
 
+    # Multi-GPU assembly of M: the fused peer-store kernel over NVLink
+    # (distributed.assemble_p2p) by default; the NCCL all-gather-v is the
+    # reference point.  The first warm-up step runs both and keeps p2p only if
+    # every rank's M is identical.
+    assembly = "none" if world == 1 else args.assembly
+    sym = SymmetricM(device, dist) if world > 1 else None
+
+    def assemble(d, mode):
+        if mode == "p2p":
+            return assemble_p2p(d, lo, hi, b.n, dist, sym, stream)
+        rp, ci, v, _, _ = eng.to_tensors(d, stream=stream)
+        return allgatherv_csr(rp, ci, v, dist)
+
     def step():
         d = eng.build(b.n, d_rp, d_ci, d_v, cfg, lo, hi, stream=stream)
         if world > 1:
-            rp, ci, v, _, _ = eng.to_tensors(d, stream=stream)
-            allgatherv_csr(rp, ci, v, dist)
+            assemble(d, assembly)
         return d
 
+    if world > 1 and assembly == "p2p":
+        d = eng.build(b.n, d_rp, d_ci, d_v, cfg, lo, hi, stream=stream)
+        ok = True
+        try:
+            prp, pci, pv = (t.clone() for t in assemble(d, "p2p"))
+        except Exception as ex:  # noqa: BLE001 — symmetric memory unavailable: use NCCL
+            print(f"p2p assembly unavailable: {ex}", file=sys.stderr)
+            ok = False
+        nrp, nci, nv = assemble(d, "nccl")
+        if ok:
+            ok = bool(torch.equal(prp, nrp) and torch.equal(pci, nci) and torch.equal(pv.view(torch.int64),
+                                                                                   nv.view(torch.int64)))
+        flag = torch.tensor([1 if ok else 0], device=device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if not flag.item():
+            assembly = "nccl"
     for _ in range(max(args.warmup, 0)):
         step()
     torch.cuda.synchronize()
@@ -295,7 +325,7 @@ def run_ours(args):
     deg_sum = eng.build(b.n, d_rp, d_ci, d_v, dcfg, lo, hi, stream=stream).stats["walk_deg_sum"]
     torch.cuda.synchronize()
     alg_bytes_local = 20 * steps_local + 8 * deg_sum
-    launches_local = sum(s["launches"] for s in stats)
+    launches_local = sum(s["launches"] for s in stats) + (args.steps if assembly == "p2p" else 0)
     agg = torch.tensor([ms_local, steps_local, walk_ms_local, alg_bytes_local, launches_local],
                        dtype=torch.float64, device=device)
     if world > 1:
@@ -380,7 +410,8 @@ def run_ours(args):
             "config": {"workload": args.config, "n": b.n, "nnz_B": b.nnz(), "epsilon": cfg.epsilon,
                        "delta": cfg.delta, "alpha": cfg.alpha, "rng_mode": args.rng,
                        "n_chains": s0["n_chains"], "max_len": s0["max_len"], "nnz_M": int(s0["nnz"]) if world == 1
-                       else None, "parallelism": f"rows/{world}" + (" + NCCL allgatherv" if world > 1 else ""),
+                       else None, "parallelism": f"rows/{world}" + ({"p2p": " + fused peer-store assembly (NVLink)",
+                                                                      "nccl": " + NCCL allgatherv"}.get(assembly, "")),
                        "l2": f"input B {(b.nnz() * 16) / 1e6:.0f} MB > 126 MB L2 (no flush)"},
             "phases_ms": {"tables": s0["ms_tables"], "walk": s0["ms_walk"], "assemble": s0["ms_assemble"],
                           "walk_kernel": s0["ms_walk_kernel"]},

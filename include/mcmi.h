@@ -176,6 +176,19 @@ int mcmi_engine_build(mcmi_engine* e, const mcmi_csr_view* b_dev, const mcmi_con
                       int64_t row_begin, int64_t row_end, void* stream, mcmi_device_csr* out,
                       mcmi_stats* stats, char* err, size_t errlen);
 
+/* Multi-GPU assembly over NVLink peer memory: stores this rank's
+ * device shard (row_ptr [rows+1] starting at 0, col_idx / values [nnz]) into
+ * each of `npeers` symmetric buffers laid out as
+ *   [row_ptr: n_total+1 int64][col_idx: nnz_total int64][values: nnz_total f64]
+ * (each array at a 16-byte boundary) at global rows [row_offset, row_offset+rows) and entries
+ * [nnz_offset, nnz_offset+nnz) (row_ptr shifted by nnz_offset).  One kernel on
+ * `stream`; the buffers are peer mappings (e.g. torch symmetric memory), the
+ * caller barriers across ranks afterwards.  Replaces an NCCL all-gather-v of
+ * the shards; rank order == row order gives the reference's assembly. */
+int mcmi_scatter_shard(const int64_t* row_ptr, const int64_t* col_idx, const double* values, int64_t rows,
+                       int64_t nnz, int64_t row_offset, int64_t nnz_offset, int64_t n_total, int64_t nnz_total,
+                       void* const* peer_buffers, int npeers, void* stream);
+
 /* ------------------------------------------------- consumer of M (§8f) */
 
 /* SolverMethod / SolverConfig (solvers.hpp:11-18) */

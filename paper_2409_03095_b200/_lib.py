@@ -23,7 +23,7 @@ EXPORTS = [
     "mcmi_engine_build", "mcmi_copy", "mcmi_version", "mcmi_solver_config_default", "mcmi_solve_device",
     "mcmi_host_register", "mcmi_host_unregister", "mcmi_from_triplets", "mcmi_mm_parse", "mcmi_mm_read_file",
     "mcmi_host_csr_get", "mcmi_host_csr_free", "mcmi_mm_format", "mcmi_mm_write_file", "mcmi_recover_inverse",
-    "mcmi_recover_inverse_device",
+    "mcmi_recover_inverse_device", "mcmi_scatter_shard",
 ]
 
 
@@ -160,5 +160,7 @@ def load(path: str | None = None):
                                        C.c_char_p, C.c_size_t]
     L.mcmi_recover_inverse_device.argtypes = [C.c_void_p, C.c_int64, C.c_void_p, C.c_int64, C.c_double, C.c_int,
                                               C.c_void_p, C.c_char_p, C.c_size_t]
+    L.mcmi_scatter_shard.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                                     C.c_int64, C.c_int64, C.c_int64, C.POINTER(C.c_void_p), C.c_int, C.c_void_p]
     _lib = L
     return L

@@ -15,7 +15,7 @@ REPO = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 LIB_DIR = os.path.join(HERE, "lib")
 LIB = os.path.join(LIB_DIR, "libmcmi.so")
-SOURCES = ["engine.cu", "tables.cu", "walk.cu", "assemble.cu", "solver.cu", "recovery.cu", "mmio.cpp"]
+SOURCES = ["engine.cu", "tables.cu", "walk.cu", "assemble.cu", "solver.cu", "recovery.cu", "scatter.cu", "mmio.cpp"]
 HEADERS = ["common.cuh", "kernels.cuh"]
 
 NVCC_FLAGS = [
