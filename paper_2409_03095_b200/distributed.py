@@ -82,11 +82,14 @@ def allgatherv_csr(row_ptr, col_idx, values, dist, group=None):
     return torch.cat(out_r), torch.cat(out_c), torch.cat(out_v)
 
 
-def build_sharded(b, cfg, dist, engine=None, device=None, stream=None, tensors=None):
+def build_sharded(b, cfg, dist, engine=None, device=None, stream=None, tensors=None, assembly="p2p", sym=None):
     """Builds this rank's row block on its GPU and assembles M on every rank.
 
     ``tensors``: B already on the device (row_ptr, col_idx, values).
-    Returns (row_ptr, col_idx, values, stats) as device tensors.
+    ``assembly``: "p2p" (fused peer-store kernel into symmetric memory; pass a
+    ``SymmetricM`` as ``sym`` to reuse its buffer across builds) or "nccl".
+    Returns (row_ptr, col_idx, values, stats) as device tensors (for "p2p",
+    views of the symmetric buffer, valid until its next assembly).
     """
     import torch
 
@@ -97,8 +100,11 @@ def build_sharded(b, cfg, dist, engine=None, device=None, stream=None, tensors=N
     rp, ci, v = tensors if tensors is not None else DeviceEngine.upload(b, dev.index)
     lo, hi = partition_rows(b.row_ptr, world)[rank]
     d = eng.build(b.n, rp, ci, v, cfg, lo, hi, stream=stream)
-    srp, sci, sv, _, _ = eng.to_tensors(d, stream=stream)
-    mrp, mci, mv = allgatherv_csr(srp, sci, sv, dist)
+    if assembly == "p2p":
+        mrp, mci, mv = assemble_p2p(d, lo, hi, b.n, dist, sym or SymmetricM(dev, dist), stream)
+    else:
+        srp, sci, sv, _, _ = eng.to_tensors(d, stream=stream)
+        mrp, mci, mv = allgatherv_csr(srp, sci, sv, dist)
     return mrp, mci, mv, d.stats
 
 
