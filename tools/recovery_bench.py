@@ -1,5 +1,6 @@
 """Recovery phase (§8f rank 4): GPU recover_inverse vs the reference's, with
-the bandwidth roofline of the rank-one update (16 n^2 bytes per update).
+its HBM traffic (16 n^2 bytes per block of 16 updates) and FP64 issue rate
+(2 n^3 multiply/add operations) against the measured peaks.
     python tools/recovery_bench.py [n ...]  -> one JSON line per n"""
 import json
 import os
@@ -22,6 +23,11 @@ def main():
     except OSError:
         pass
     hbm = float(peaks.get("hbm_gbs", 6544.0)) if isinstance(peaks, dict) else 6544.0
+    try:  # measured by tools/fp64_peak.cu (DMUL + DADD issue rate)
+        fp64 = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "profiles",
+                                           "fp64_peak.json")))["fp64_mul_add_ops_per_s"]
+    except (OSError, KeyError, ValueError):
+        fp64 = 1.85e13
     for n in [int(x) for x in sys.argv[1:]] or [1024, 2048, 4096]:
         rng = np.random.default_rng(n)
         m = rng.uniform(-1, 1, (n, n)) / n + np.eye(n)
@@ -54,10 +60,14 @@ def main():
         exact = bool(np.array_equal(got_k.view(np.uint64), want_k.view(np.uint64)))
         if n <= 1024:
             exact = exact and bool(np.array_equal(got.view(np.uint64), ref.recover_inverse(m, s).view(np.uint64)))
-        gbs = 16.0 * n * n * n / (best / 1e3) / 1e9
+        # the kernel moves 16 n^2 bytes per block of 16 updates and issues 2 n^3
+        # FP64 operations (one multiply and one add per element update, no FMA)
+        gbs = 16.0 * n * n * ((n + 15) // 16) / (best / 1e3) / 1e9
+        ops = 2.0 * n ** 3 / (best / 1e3)
         print(json.dumps({"n": n, "updates": n, "device_ms": round(best, 3), "host_api_ms": round(host_ms, 1),
                           "ref_ms_est": round(ref_ms, 1), "ref_sample_updates": k, "bit_exact": exact,
-                          "achieved_gbs": round(gbs, 1), "hbm_peak_gbs": hbm, "frac_hbm": round(gbs / hbm, 3),
+                          "hbm_gbs": round(gbs, 1), "frac_hbm": round(gbs / hbm, 3),
+                          "fp64_ops_per_s": ops, "frac_fp64": round(ops / fp64, 3),
                           "speedup_vs_ref": round(ref_ms / best, 1)}), flush=True)
 
 
