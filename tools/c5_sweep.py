@@ -31,7 +31,6 @@ def main():
     p.add_argument("--chains", default="100,1000,10000,100000")
     p.add_argument("--lens", default="4,8,16,32,64")
     a = p.parse_args()
-    import torch
     from paper_2409_03095_b200 import generators as G
     from paper_2409_03095_b200.engine import DeviceEngine
     from paper_2409_03095_b200.mcspai import McConfig, RngMode
