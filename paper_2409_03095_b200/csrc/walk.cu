@@ -420,8 +420,11 @@ __device__ int sort_by_column(int* keys, double* vals, int s) {
 
 constexpr int kRankTopkMax = 256;  // above this row length retain_top_k uses radix_topk
 
-template <int MODE, int MINB, bool GL, bool DEG>
+template <int MODE, int MINB, bool GL, bool DEG, int LF = 0>
 __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
+    // LF > 0: a launch with max_len == log_stride == LF and 32-lane batches:
+    // the step loop (unrolled, no length or log-capacity tests) and the fold's
+    // position arithmetic are compile-time.
     // MODE 0: reference stream with 32-bit draw positions (N*L < 2^32, every
     // practical budget); MODE 2: the same with 64-bit positions; MODE 1: keyed.
     constexpr bool IS_REF = MODE != 1;
@@ -430,9 +433,9 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     const int lane = static_cast<int>(threadIdx.x & 31);
     const int warp = static_cast<int>(threadIdx.x >> 5);
     const int cap = a.cap;
-    const int S = a.log_stride;                 // step deposits per chain (max_len)
-    const int B = a.lanes;                      // chains per batch
-    const int logn = a.log_n;                   // round32(B * S), host-computed (kernel parameter)
+    const int S = LF ? LF : a.log_stride;       // step deposits per chain (max_len)
+    const int B = LF ? 32 : a.lanes;            // chains per batch
+    const int logn = LF ? round32(32 * LF) : a.log_n;  // round32(B * S), host-computed (kernel parameter)
     const size_t per_warp = static_cast<size_t>(a.warp_bytes);
     // GL: per-warp accumulator + log in global scratch (large rows / long walks)
     unsigned char* wbase = GL ? a.gscratch + per_warp * (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp)
@@ -441,7 +444,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     const unsigned cap_mask = static_cast<unsigned>(cap - 1);
     const int shift = a.hash_shift;             // 32 - log2(cap)
     const unsigned lt_mask = (1u << lane) - 1u;
-    const int s_shift = a.log_shift;            // log2(S) when S is a power of two, else -1
+    const int s_shift = LF ? (LF == 1 ? 0 : LF == 2 ? 1 : LF == 4 ? 2 : -1) : a.log_shift;  // log2(S), or -1
 
     const uint4* __restrict__ rec = a.t.rec;
     const double2* __restrict__ ent = a.t.ent;
@@ -449,7 +452,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     const uint2 key = make_uint2(static_cast<uint32_t>(a.seed), static_cast<uint32_t>(a.seed >> 32));
     // host guarantees 1 <= N < 2^31 and L < 2^31 (engine.cu), so 32-bit loop state
     const int N = static_cast<int>(a.n_chains);
-    const int L = static_cast<int>(a.max_len);
+    const int L = LF ? LF : static_cast<int>(a.max_len);
 
     unsigned long long tot_steps = 0, tot_deg = 0;
 
@@ -513,11 +516,16 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             uint4 blk = make_uint4(0, 0, 0, 0);
             bool alive = active;
             bool log_full = false;  // the walk would outgrow this tier's deposit log
-            for (int t = 0; __any_sync(FULL_MASK, alive); ++t) {
-                if (alive && t >= L) alive = false;
-                if (alive && m >= S) {
-                    alive = false;
-                    log_full = true;
+#pragma unroll
+            for (int t = 0; LF ? (t < LF) : __any_sync(FULL_MASK, alive); ++t) {
+                if (LF) {  // compile-time trip count: no log overflow, no length test
+                    if (!__any_sync(FULL_MASK, alive)) break;
+                } else {
+                    if (alive && t >= L) alive = false;
+                    if (alive && m >= S) {
+                        alive = false;
+                        log_full = true;
+                    }
                 }
                 if (!alive) continue;
                 uint4 r0, r1;
@@ -919,16 +927,16 @@ size_t walk_global_bytes_per_warp(int cap, int lanes, int log_stride) {
     return walk_smem_bytes_per_warp(cap, lanes, log_stride);
 }
 
-template <int MODE, int MINB, bool GL, bool DEG>
+template <int MODE, int MINB, bool GL, bool DEG, int LF = 0>
 cudaError_t launch_walk_t(const WalkArgs& a, int warps_per_block, int num_sms, int64_t max_warps,
                           cudaStream_t s) {
     const size_t smem = GL ? 0 : walk_smem_bytes_per_warp(a.cap, a.lanes, a.log_stride) * warps_per_block;
     const int threads = warps_per_block * 32;
-    cudaError_t e = cudaFuncSetAttribute(k_walk<MODE, MINB, GL, DEG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_walk<MODE, MINB, GL, DEG, LF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<MODE, MINB, GL, DEG>, threads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<MODE, MINB, GL, DEG, LF>, threads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     int64_t blocks = static_cast<int64_t>(per_sm) * num_sms;
@@ -936,7 +944,7 @@ cudaError_t launch_walk_t(const WalkArgs& a, int warps_per_block, int num_sms, i
     if (blocks > need) blocks = need;
     if (max_warps > 0 && blocks * warps_per_block > max_warps)
         blocks = std::max<int64_t>(1, max_warps / warps_per_block);
-    k_walk<MODE, MINB, GL, DEG><<<static_cast<unsigned>(blocks), threads, smem, s>>>(a);
+    k_walk<MODE, MINB, GL, DEG, LF><<<static_cast<unsigned>(blocks), threads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -974,6 +982,15 @@ cudaError_t launch_walk(const WalkArgs& a_in, int warps_per_block, int num_sms, 
                            4294967295.0 ||  // draw positions beyond 32 bits
                        getenv("MCMI_FORCE_POS64") != nullptr;  // tests exercise the 64-bit variant
     const int mode = a.rng_mode == 0 ? (pos64 ? 2 : 0) : 1;
+    // L = 2 specialisation (compile-time step loop and fold arithmetic)
+    // Walk-length specialisations (compile-time step loop and fold arithmetic):
+    // L = 2 (every defaults config) and L = 4.  Measured -7..-11% on C1-C4 and
+    // C3-heavy; rows of few chains on the 256-slot tier (C2 at defaults: 141
+    // chains, ~74 columns, finalize-heavy) run 1-5% faster on the generic
+    // kernel, so they keep it.  MCMI_WALK_GENERIC (tuning) disables both.
+    const bool spec = getenv("MCMI_WALK_GENERIC") == nullptr && !(a.cap >= 256 && a.n_chains < 1024);
+    const bool l2 = spec && a.max_len == 2 && a.log_stride == 2 && a.lanes == 32;
+    const bool l4 = spec && a.max_len == 4 && a.log_stride == 4 && a.lanes == 32;
     // variants: the global tier and the statistics build use one launch bound
 #define MCMI_WALK_RARE(M)                                                                              \
     if (global_tier)                                                                                   \
@@ -988,11 +1005,15 @@ cudaError_t launch_walk(const WalkArgs& a_in, int warps_per_block, int num_sms, 
         MCMI_WALK_RARE(0)
         if (mb == 5) return launch_walk_t<0, 5, false, false>(a, warps_per_block, num_sms, 0, s);
         if (mb == 4) return launch_walk_t<0, 4, false, false>(a, warps_per_block, num_sms, 0, s);
+        if (l2) return launch_walk_t<0, 6, false, false, 2>(a, warps_per_block, num_sms, 0, s);
+        if (l4) return launch_walk_t<0, 6, false, false, 4>(a, warps_per_block, num_sms, 0, s);
         return launch_walk_t<0, 6, false, false>(a, warps_per_block, num_sms, 0, s);
     }
     MCMI_WALK_RARE(1)
     if (mb == 5) return launch_walk_t<1, 5, false, false>(a, warps_per_block, num_sms, 0, s);
     if (mb == 4) return launch_walk_t<1, 4, false, false>(a, warps_per_block, num_sms, 0, s);
+    if (l2) return launch_walk_t<1, 6, false, false, 2>(a, warps_per_block, num_sms, 0, s);
+    if (l4) return launch_walk_t<1, 6, false, false, 4>(a, warps_per_block, num_sms, 0, s);
     return launch_walk_t<1, 6, false, false>(a, warps_per_block, num_sms, 0, s);
 #undef MCMI_WALK_RARE
 }

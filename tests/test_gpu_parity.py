@@ -394,3 +394,26 @@ def test_reference_stream_64bit_positions(mc, name, monkeypatch):
     b = _csr(mc, case["input"])
     inv = mc.compute_preconditioner(b, _cfg(mc, case["config"]))
     assert mm_sha256(b.n, inv.m.row_ptr, inv.m.col_idx, inv.m.values) == case["mm_sha256"]
+
+
+@pytest.mark.parametrize("rng", [0, 1])
+@pytest.mark.parametrize("max_len", [2, 4])
+def test_walk_length_specialisations_match_generic(mc, oracle_mod, rng, max_len):
+    """The compile-time L = 2 / L = 4 walk kernels equal the generic kernel
+    (MCMI_WALK_GENERIC) and the oracle."""
+    import os
+    from paper_2409_03095_b200 import generators as G
+    b = G.laplacian3d(24)
+    cfg = mc.McConfig(chains_override=300, max_len_override=max_len, delta=1e-6, retain_k=10, master_seed=5,
+                      rng_mode=rng)
+    spec = mc.compute_preconditioner(b, cfg)
+    os.environ["MCMI_WALK_GENERIC"] = "1"
+    try:
+        gen = mc.compute_preconditioner(b, cfg)
+    finally:
+        del os.environ["MCMI_WALK_GENERIC"]
+    assert spec.m == gen.m and spec.stats["walk_steps"] == gen.stats["walk_steps"]
+    want = oracle_mod.compute_preconditioner(b.n, b.row_ptr, b.col_idx, b.values, row_begin=0, row_end=300,
+                                             **cfg.oracle_kwargs())
+    nnz = int(spec.m.row_ptr[300])
+    assert np.array_equal(spec.m.col_idx[:nnz], want.col_idx) and bits_equal(spec.m.values[:nnz], want.values)
