@@ -420,7 +420,7 @@ __device__ int sort_by_column(int* keys, double* vals, int s) {
 
 constexpr int kRankTopkMax = 256;  // above this row length retain_top_k uses radix_topk
 
-template <int MODE, int MINB, bool GL, bool DEG, int LF = 0>
+template <int MODE, int MINB, bool GL, bool DEG, int LF = 0, int CAPC = 0>
 __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     // LF > 0: a launch with max_len == log_stride == LF and 32-lane batches:
     // the step loop (unrolled, no length or log-capacity tests) and the fold's
@@ -432,17 +432,18 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = static_cast<int>(threadIdx.x & 31);
     const int warp = static_cast<int>(threadIdx.x >> 5);
-    const int cap = a.cap;
+    const int cap = CAPC ? CAPC : a.cap;  // CAPC: compile-time hash capacity (tiers 32, 64, 256)
     const int S = LF ? LF : a.log_stride;       // step deposits per chain (max_len)
     const int B = LF ? 32 : a.lanes;            // chains per batch
     const int logn = LF ? round32(32 * LF) : a.log_n;  // round32(B * S), host-computed (kernel parameter)
-    const size_t per_warp = static_cast<size_t>(a.warp_bytes);
+    const size_t per_warp = (LF && CAPC) ? static_cast<size_t>(CAPC + logn) * 12 + 0
+                                         : static_cast<size_t>(a.warp_bytes);
     // GL: per-warp accumulator + log in global scratch (large rows / long walks)
     unsigned char* wbase = GL ? a.gscratch + per_warp * (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp)
                               : smem_raw + per_warp * warp;
     const WarpSmem sm = carve(wbase, cap, logn);
     const unsigned cap_mask = static_cast<unsigned>(cap - 1);
-    const int shift = a.hash_shift;             // 32 - log2(cap)
+    const int shift = CAPC ? 32 - (31 - __clz(CAPC)) : a.hash_shift;  // 32 - log2(cap)
     const unsigned lt_mask = (1u << lane) - 1u;
     const int s_shift = LF ? (LF == 1 ? 0 : LF == 2 ? 1 : LF == 4 ? 2 : -1) : a.log_shift;  // log2(S), or -1
 
@@ -485,7 +486,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
         unsigned long long row_steps = 0, row_deg = 0;
         // reference-stream speculation state
         PosT D = 0;
-        unsigned ell = static_cast<unsigned>(a.ell0);
+        unsigned ell = LF ? static_cast<unsigned>(LF < 2 ? LF : 2) : static_cast<unsigned>(a.ell0);
         bool row_done = false;
 
         while (!row_done) {
@@ -771,7 +772,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 __syncwarp();
             }
             distinct += warp_sum_int(n_new);
-            if (__any_sync(FULL_MASK, fail) || distinct > a.cap_limit) {
+            if (__any_sync(FULL_MASK, fail) || distinct > (CAPC ? CAPC - CAPC / 4 : a.cap_limit)) {
                 overflow = true;
                 break;
             }
@@ -927,16 +928,16 @@ size_t walk_global_bytes_per_warp(int cap, int lanes, int log_stride) {
     return walk_smem_bytes_per_warp(cap, lanes, log_stride);
 }
 
-template <int MODE, int MINB, bool GL, bool DEG, int LF = 0>
+template <int MODE, int MINB, bool GL, bool DEG, int LF = 0, int CAPC = 0>
 cudaError_t launch_walk_t(const WalkArgs& a, int warps_per_block, int num_sms, int64_t max_warps,
                           cudaStream_t s) {
     const size_t smem = GL ? 0 : walk_smem_bytes_per_warp(a.cap, a.lanes, a.log_stride) * warps_per_block;
     const int threads = warps_per_block * 32;
-    cudaError_t e = cudaFuncSetAttribute(k_walk<MODE, MINB, GL, DEG, LF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_walk<MODE, MINB, GL, DEG, LF, CAPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<MODE, MINB, GL, DEG, LF>, threads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<MODE, MINB, GL, DEG, LF, CAPC>, threads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     int64_t blocks = static_cast<int64_t>(per_sm) * num_sms;
@@ -944,7 +945,7 @@ cudaError_t launch_walk_t(const WalkArgs& a, int warps_per_block, int num_sms, i
     if (blocks > need) blocks = need;
     if (max_warps > 0 && blocks * warps_per_block > max_warps)
         blocks = std::max<int64_t>(1, max_warps / warps_per_block);
-    k_walk<MODE, MINB, GL, DEG, LF><<<static_cast<unsigned>(blocks), threads, smem, s>>>(a);
+    k_walk<MODE, MINB, GL, DEG, LF, CAPC><<<static_cast<unsigned>(blocks), threads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -1005,15 +1006,31 @@ cudaError_t launch_walk(const WalkArgs& a_in, int warps_per_block, int num_sms, 
         MCMI_WALK_RARE(0)
         if (mb == 5) return launch_walk_t<0, 5, false, false>(a, warps_per_block, num_sms, 0, s);
         if (mb == 4) return launch_walk_t<0, 4, false, false>(a, warps_per_block, num_sms, 0, s);
-        if (l2) return launch_walk_t<0, 6, false, false, 2>(a, warps_per_block, num_sms, 0, s);
-        if (l4) return launch_walk_t<0, 6, false, false, 4>(a, warps_per_block, num_sms, 0, s);
+        if (l2) {
+            if (a.cap == 32) return launch_walk_t<0, 6, false, false, 2, 32>(a, warps_per_block, num_sms, 0, s);
+            if (a.cap == 64) return launch_walk_t<0, 6, false, false, 2, 64>(a, warps_per_block, num_sms, 0, s);
+            if (a.cap == 256) return launch_walk_t<0, 6, false, false, 2, 256>(a, warps_per_block, num_sms, 0, s);
+            return launch_walk_t<0, 6, false, false, 2>(a, warps_per_block, num_sms, 0, s);
+        }
+        if (l4) {
+            if (a.cap == 256) return launch_walk_t<0, 6, false, false, 4, 256>(a, warps_per_block, num_sms, 0, s);
+            return launch_walk_t<0, 6, false, false, 4>(a, warps_per_block, num_sms, 0, s);
+        }
         return launch_walk_t<0, 6, false, false>(a, warps_per_block, num_sms, 0, s);
     }
     MCMI_WALK_RARE(1)
     if (mb == 5) return launch_walk_t<1, 5, false, false>(a, warps_per_block, num_sms, 0, s);
     if (mb == 4) return launch_walk_t<1, 4, false, false>(a, warps_per_block, num_sms, 0, s);
-    if (l2) return launch_walk_t<1, 6, false, false, 2>(a, warps_per_block, num_sms, 0, s);
-    if (l4) return launch_walk_t<1, 6, false, false, 4>(a, warps_per_block, num_sms, 0, s);
+    if (l2) {
+        if (a.cap == 32) return launch_walk_t<1, 6, false, false, 2, 32>(a, warps_per_block, num_sms, 0, s);
+        if (a.cap == 64) return launch_walk_t<1, 6, false, false, 2, 64>(a, warps_per_block, num_sms, 0, s);
+        if (a.cap == 256) return launch_walk_t<1, 6, false, false, 2, 256>(a, warps_per_block, num_sms, 0, s);
+        return launch_walk_t<1, 6, false, false, 2>(a, warps_per_block, num_sms, 0, s);
+    }
+    if (l4) {
+        if (a.cap == 256) return launch_walk_t<1, 6, false, false, 4, 256>(a, warps_per_block, num_sms, 0, s);
+        return launch_walk_t<1, 6, false, false, 4>(a, warps_per_block, num_sms, 0, s);
+    }
     return launch_walk_t<1, 6, false, false>(a, warps_per_block, num_sms, 0, s);
 #undef MCMI_WALK_RARE
 }
