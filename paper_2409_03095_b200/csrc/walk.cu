@@ -984,12 +984,12 @@ cudaError_t launch_walk(const WalkArgs& a_in, int warps_per_block, int num_sms, 
                        getenv("MCMI_FORCE_POS64") != nullptr;  // tests exercise the 64-bit variant
     const int mode = a.rng_mode == 0 ? (pos64 ? 2 : 0) : 1;
     // L = 2 specialisation (compile-time step loop and fold arithmetic)
-    // Walk-length specialisations (compile-time step loop and fold arithmetic):
-    // L = 2 (every defaults config) and L = 4.  Measured -7..-11% on C1-C4 and
-    // C3-heavy; rows of few chains on the 256-slot tier (C2 at defaults: 141
-    // chains, ~74 columns, finalize-heavy) run 1-5% faster on the generic
-    // kernel, so they keep it.  MCMI_WALK_GENERIC (tuning) disables both.
-    const bool spec = getenv("MCMI_WALK_GENERIC") == nullptr && !(a.cap >= 256 && a.n_chains < 1024);
+    // Walk-length specialisations (compile-time step loop and fold arithmetic,
+    // plus compile-time hash capacity for the 32/64/256-slot tiers): L = 2
+    // (every defaults config) and L = 4.  Measured -8..-14% on C1-C4 and
+    // C3-heavy against the generic kernel.  MCMI_WALK_GENERIC (tuning) disables
+    // them.
+    const bool spec = getenv("MCMI_WALK_GENERIC") == nullptr;
     const bool l2 = spec && a.max_len == 2 && a.log_stride == 2 && a.lanes == 32;
     const bool l4 = spec && a.max_len == 4 && a.log_stride == 4 && a.lanes == 32;
     // variants: the global tier and the statistics build use one launch bound
