@@ -445,7 +445,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     const unsigned cap_mask = static_cast<unsigned>(cap - 1);
     const int shift = CAPC ? 32 - (31 - __clz(CAPC)) : a.hash_shift;  // 32 - log2(cap)
     const unsigned lt_mask = (1u << lane) - 1u;
-    const int s_shift = LF ? (LF == 1 ? 0 : LF == 2 ? 1 : LF == 4 ? 2 : -1) : a.log_shift;  // log2(S), or -1
+    const int s_shift = LF ? (LF == 1 ? 0 : LF == 2 ? 1 : LF == 4 ? 2 : LF == 8 ? 3 : -1) : a.log_shift;  // log2(S), or -1
 
     const uint4* __restrict__ rec = a.t.rec;
     const double2* __restrict__ ent = a.t.ent;
@@ -986,12 +986,13 @@ cudaError_t launch_walk(const WalkArgs& a_in, int warps_per_block, int num_sms, 
     // L = 2 specialisation (compile-time step loop and fold arithmetic)
     // Walk-length specialisations (compile-time step loop and fold arithmetic,
     // plus compile-time hash capacity for the 32/64/256-slot tiers): L = 2
-    // (every defaults config) and L = 4.  Measured -8..-14% on C1-C4 and
-    // C3-heavy against the generic kernel.  MCMI_WALK_GENERIC (tuning) disables
-    // them.
+    // (every defaults config), 3, 4 and 8 (C5).  Measured -2..-14% against the
+    // generic kernel.  MCMI_WALK_GENERIC (tuning) disables them.
     const bool spec = getenv("MCMI_WALK_GENERIC") == nullptr;
     const bool l2 = spec && a.max_len == 2 && a.log_stride == 2 && a.lanes == 32;
     const bool l4 = spec && a.max_len == 4 && a.log_stride == 4 && a.lanes == 32;
+    const bool l3 = spec && a.max_len == 3 && a.log_stride == 3 && a.lanes == 32;
+    const bool l8 = spec && a.max_len == 8 && a.log_stride == 8 && a.lanes == 32;
     // variants: the global tier and the statistics build use one launch bound
 #define MCMI_WALK_RARE(M)                                                                              \
     if (global_tier)                                                                                   \
@@ -1016,6 +1017,14 @@ cudaError_t launch_walk(const WalkArgs& a_in, int warps_per_block, int num_sms, 
             if (a.cap == 256) return launch_walk_t<0, 6, false, false, 4, 256>(a, warps_per_block, num_sms, 0, s);
             return launch_walk_t<0, 6, false, false, 4>(a, warps_per_block, num_sms, 0, s);
         }
+        if (l3) {
+            if (a.cap == 256) return launch_walk_t<0, 6, false, false, 3, 256>(a, warps_per_block, num_sms, 0, s);
+            return launch_walk_t<0, 6, false, false, 3>(a, warps_per_block, num_sms, 0, s);
+        }
+        if (l8) {
+            if (a.cap == 256) return launch_walk_t<0, 6, false, false, 8, 256>(a, warps_per_block, num_sms, 0, s);
+            return launch_walk_t<0, 6, false, false, 8>(a, warps_per_block, num_sms, 0, s);
+        }
         return launch_walk_t<0, 6, false, false>(a, warps_per_block, num_sms, 0, s);
     }
     MCMI_WALK_RARE(1)
@@ -1030,6 +1039,14 @@ cudaError_t launch_walk(const WalkArgs& a_in, int warps_per_block, int num_sms, 
     if (l4) {
         if (a.cap == 256) return launch_walk_t<1, 6, false, false, 4, 256>(a, warps_per_block, num_sms, 0, s);
         return launch_walk_t<1, 6, false, false, 4>(a, warps_per_block, num_sms, 0, s);
+    }
+    if (l3) {
+        if (a.cap == 256) return launch_walk_t<1, 6, false, false, 3, 256>(a, warps_per_block, num_sms, 0, s);
+        return launch_walk_t<1, 6, false, false, 3>(a, warps_per_block, num_sms, 0, s);
+    }
+    if (l8) {
+        if (a.cap == 256) return launch_walk_t<1, 6, false, false, 8, 256>(a, warps_per_block, num_sms, 0, s);
+        return launch_walk_t<1, 6, false, false, 8>(a, warps_per_block, num_sms, 0, s);
     }
     return launch_walk_t<1, 6, false, false>(a, warps_per_block, num_sms, 0, s);
 #undef MCMI_WALK_RARE

@@ -397,10 +397,10 @@ def test_reference_stream_64bit_positions(mc, name, monkeypatch):
 
 
 @pytest.mark.parametrize("rng", [0, 1])
-@pytest.mark.parametrize("max_len", [2, 4])
+@pytest.mark.parametrize("max_len", [2, 3, 4, 8])
 def test_walk_length_specialisations_match_generic(mc, oracle_mod, rng, max_len):
-    """The compile-time L = 2 / L = 4 walk kernels equal the generic kernel
-    (MCMI_WALK_GENERIC) and the oracle."""
+    """The compile-time L = 2 / 3 / 4 / 8 walk kernels equal the generic
+    kernel (MCMI_WALK_GENERIC) and the oracle."""
     import os
     from paper_2409_03095_b200 import generators as G
     b = G.laplacian3d(24)
