@@ -25,6 +25,8 @@
 //   read_matrix_market_file<CsrMatrix, ParseError>(path)     matrix_market.cpp:149-153
 //   write_matrix_market(m, ostream&)                         matrix_market.cpp:155-169
 //   write_matrix_market_file(m, path)                        matrix_market.cpp:171-177
+// §8f rank 4:
+//   recover_inverse<DenseMatrix, RecoveryError>(m, plan, tol) recovery.cpp:7-33
 #ifndef MCMI_MCSPAI_COMPAT_HPP
 #define MCMI_MCSPAI_COMPAT_HPP
 
@@ -208,6 +210,17 @@ void write_matrix_market_file(const CsrT& m, const std::string& path) {
     char err[512] = {0};
     const int code = mcmi_mm_write_file(&v, path.c_str(), err, sizeof err);
     if (code != MCMI_OK) detail::rethrow_io<std::runtime_error>(code, err);
+}
+
+template <class DenseT, class RecoveryErrorT, class PlanT>
+DenseT recover_inverse(const DenseT& b_hat_inv, const PlanT& plan, double tol = 1e-12, const Options& opt = {}) {
+    DenseT out = b_hat_inv;
+    char err[512] = {0};
+    const int code = mcmi_recover_inverse(out.values.data(), static_cast<int64_t>(out.n), plan.s_diag.data(),
+                                          static_cast<int64_t>(plan.s_diag.size()), tol, opt.device, err, sizeof err);
+    if (code == MCMI_ERECOVERY) throw RecoveryErrorT(err);
+    if (code != MCMI_OK) detail::rethrow_io<std::runtime_error>(code, err);
+    return out;
 }
 
 }  // namespace compat

@@ -15,6 +15,9 @@
 #include "mcmi/mcspai_compat.hpp"
 #include "mcspai/matrix_market.hpp"
 #include "mcspai/mc_engine.hpp"
+#include "mcspai/recovery.hpp"
+#include "mcspai/dense_solve.hpp"
+#include "mcspai/split.hpp"
 #include "mcspai/synthetic.hpp"
 
 using namespace mcspai;
@@ -109,6 +112,17 @@ int main(int argc, char** argv) {
         ok = false;
     } catch (const SplitError& e) {
         std::printf("[PASS] SplitError: %s\n", e.what());
+    }
+    // recovery phase (§8f rank 4): recover_inverse on the reference's DenseMatrix
+    {
+        const CsrMatrix b = make_random_ddm(120, 0.1, 5);
+        const SplitSystem sys = augment_and_split(b, 1.5, AugmentationMode::sign_aware);
+        const DenseMatrix bhi = dense_inverse(csr_to_dense(sys.b_hat));
+        const DenseMatrix r1 = recover_inverse(bhi, {sys.s_diag});
+        const DenseMatrix r2 = mcmi::compat::recover_inverse<DenseMatrix, RecoveryError>(bhi, RecoveryPlan{sys.s_diag});
+        const bool same = r1.values == r2.values;
+        std::printf("[%s] recover_inverse n=%lld bit-identical\n", same ? "PASS" : "FAIL", static_cast<long long>(b.n));
+        ok &= same;
     }
     return ok ? 0 : 1;
 }
