@@ -1023,6 +1023,7 @@ cudaError_t launch_walk(const WalkArgs& a_in, int warps_per_block, int num_sms, 
         }
         if (l8) {
             if (a.cap == 256) return launch_walk_t<0, 6, false, false, 8, 256>(a, warps_per_block, num_sms, 0, s);
+            if (a.cap == 1024) return launch_walk_t<0, 6, false, false, 8, 1024>(a, warps_per_block, num_sms, 0, s);
             return launch_walk_t<0, 6, false, false, 8>(a, warps_per_block, num_sms, 0, s);
         }
         return launch_walk_t<0, 6, false, false>(a, warps_per_block, num_sms, 0, s);
@@ -1046,6 +1047,7 @@ cudaError_t launch_walk(const WalkArgs& a_in, int warps_per_block, int num_sms, 
     }
     if (l8) {
         if (a.cap == 256) return launch_walk_t<1, 6, false, false, 8, 256>(a, warps_per_block, num_sms, 0, s);
+        if (a.cap == 1024) return launch_walk_t<1, 6, false, false, 8, 1024>(a, warps_per_block, num_sms, 0, s);
         return launch_walk_t<1, 6, false, false, 8>(a, warps_per_block, num_sms, 0, s);
     }
     return launch_walk_t<1, 6, false, false>(a, warps_per_block, num_sms, 0, s);
