@@ -436,7 +436,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     const int S = LF ? LF : a.log_stride;       // step deposits per chain (max_len)
     const int B = LF ? 32 : a.lanes;            // chains per batch
     const int logn = LF ? round32(32 * LF) : a.log_n;  // round32(B * S), host-computed (kernel parameter)
-    const size_t per_warp = (LF && CAPC) ? static_cast<size_t>(CAPC + logn) * 12 + 0
+    const size_t per_warp = (LF && CAPC) ? static_cast<size_t>(CAPC + logn) * 12  // walk_smem_bytes_per_warp
                                          : static_cast<size_t>(a.warp_bytes);
     // GL: per-warp accumulator + log in global scratch (large rows / long walks)
     unsigned char* wbase = GL ? a.gscratch + per_warp * (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp)
@@ -960,6 +960,36 @@ int walk_minb() {
     return v;
 }
 
+// The compile-time (walk length, capacity) variants of k_walk for MODE 0 / 1;
+// false if none fits this launch (lanes must be 32 and log_stride == L).
+template <int MODE>
+bool launch_specialised(const WalkArgs& a, int wpb, int sms, cudaStream_t s, cudaError_t* err) {
+    if (a.lanes != 32 || a.log_stride != a.max_len) return false;
+    switch (a.max_len) {
+        case 2:
+            *err = a.cap == 32    ? launch_walk_t<MODE, 6, false, false, 2, 32>(a, wpb, sms, 0, s)
+                   : a.cap == 64  ? launch_walk_t<MODE, 6, false, false, 2, 64>(a, wpb, sms, 0, s)
+                   : a.cap == 256 ? launch_walk_t<MODE, 6, false, false, 2, 256>(a, wpb, sms, 0, s)
+                                  : launch_walk_t<MODE, 6, false, false, 2>(a, wpb, sms, 0, s);
+            return true;
+        case 3:
+            *err = a.cap == 256 ? launch_walk_t<MODE, 6, false, false, 3, 256>(a, wpb, sms, 0, s)
+                                : launch_walk_t<MODE, 6, false, false, 3>(a, wpb, sms, 0, s);
+            return true;
+        case 4:
+            *err = a.cap == 256 ? launch_walk_t<MODE, 6, false, false, 4, 256>(a, wpb, sms, 0, s)
+                                : launch_walk_t<MODE, 6, false, false, 4>(a, wpb, sms, 0, s);
+            return true;
+        case 8:
+            *err = a.cap == 256    ? launch_walk_t<MODE, 6, false, false, 8, 256>(a, wpb, sms, 0, s)
+                   : a.cap == 1024 ? launch_walk_t<MODE, 6, false, false, 8, 1024>(a, wpb, sms, 0, s)
+                                   : launch_walk_t<MODE, 6, false, false, 8>(a, wpb, sms, 0, s);
+            return true;
+        default:
+            return false;
+    }
+}
+
 cudaError_t launch_walk(const WalkArgs& a_in, int warps_per_block, int num_sms, bool global_tier,
                         int64_t max_warps, cudaStream_t s) {
     if (a_in.n_work <= 0) return cudaSuccess;
@@ -983,75 +1013,38 @@ cudaError_t launch_walk(const WalkArgs& a_in, int warps_per_block, int num_sms, 
                            4294967295.0 ||  // draw positions beyond 32 bits
                        getenv("MCMI_FORCE_POS64") != nullptr;  // tests exercise the 64-bit variant
     const int mode = a.rng_mode == 0 ? (pos64 ? 2 : 0) : 1;
-    // L = 2 specialisation (compile-time step loop and fold arithmetic)
     // Walk-length specialisations (compile-time step loop and fold arithmetic,
-    // plus compile-time hash capacity for the 32/64/256-slot tiers): L = 2
-    // (every defaults config), 3, 4 and 8 (C5).  Measured -2..-14% against the
-    // generic kernel.  MCMI_WALK_GENERIC (tuning) disables them.
+    // plus compile-time hash capacity for the common tiers): L = 2 (every
+    // defaults config), 3, 4 and 8 (C5).  Measured -2..-14% against the generic
+    // kernel.  MCMI_WALK_GENERIC (tuning) disables them.
     const bool spec = getenv("MCMI_WALK_GENERIC") == nullptr;
-    const bool l2 = spec && a.max_len == 2 && a.log_stride == 2 && a.lanes == 32;
-    const bool l4 = spec && a.max_len == 4 && a.log_stride == 4 && a.lanes == 32;
-    const bool l3 = spec && a.max_len == 3 && a.log_stride == 3 && a.lanes == 32;
-    const bool l8 = spec && a.max_len == 8 && a.log_stride == 8 && a.lanes == 32;
+    cudaError_t se = cudaSuccess;
     // variants: the global tier and the statistics build use one launch bound
-#define MCMI_WALK_RARE(M)                                                                              \
-    if (global_tier)                                                                                   \
-        return a.deg_stats ? launch_walk_t<M, 4, true, true>(a, warps_per_block, num_sms, max_warps, s) \
-                           : launch_walk_t<M, 4, true, false>(a, warps_per_block, num_sms, max_warps, s); \
-    if (a.deg_stats) return launch_walk_t<M, 6, false, true>(a, warps_per_block, num_sms, 0, s);
     if (mode == 2) {
-        MCMI_WALK_RARE(2)
+        if (global_tier)
+            return a.deg_stats ? launch_walk_t<2, 4, true, true>(a, warps_per_block, num_sms, max_warps, s)
+                               : launch_walk_t<2, 4, true, false>(a, warps_per_block, num_sms, max_warps, s);
+        if (a.deg_stats) return launch_walk_t<2, 6, false, true>(a, warps_per_block, num_sms, 0, s);
         return launch_walk_t<2, 6, false, false>(a, warps_per_block, num_sms, 0, s);
     }
     if (mode == 0) {
-        MCMI_WALK_RARE(0)
+        if (global_tier)
+            return a.deg_stats ? launch_walk_t<0, 4, true, true>(a, warps_per_block, num_sms, max_warps, s)
+                               : launch_walk_t<0, 4, true, false>(a, warps_per_block, num_sms, max_warps, s);
+        if (a.deg_stats) return launch_walk_t<0, 6, false, true>(a, warps_per_block, num_sms, 0, s);
         if (mb == 5) return launch_walk_t<0, 5, false, false>(a, warps_per_block, num_sms, 0, s);
         if (mb == 4) return launch_walk_t<0, 4, false, false>(a, warps_per_block, num_sms, 0, s);
-        if (l2) {
-            if (a.cap == 32) return launch_walk_t<0, 6, false, false, 2, 32>(a, warps_per_block, num_sms, 0, s);
-            if (a.cap == 64) return launch_walk_t<0, 6, false, false, 2, 64>(a, warps_per_block, num_sms, 0, s);
-            if (a.cap == 256) return launch_walk_t<0, 6, false, false, 2, 256>(a, warps_per_block, num_sms, 0, s);
-            return launch_walk_t<0, 6, false, false, 2>(a, warps_per_block, num_sms, 0, s);
-        }
-        if (l4) {
-            if (a.cap == 256) return launch_walk_t<0, 6, false, false, 4, 256>(a, warps_per_block, num_sms, 0, s);
-            return launch_walk_t<0, 6, false, false, 4>(a, warps_per_block, num_sms, 0, s);
-        }
-        if (l3) {
-            if (a.cap == 256) return launch_walk_t<0, 6, false, false, 3, 256>(a, warps_per_block, num_sms, 0, s);
-            return launch_walk_t<0, 6, false, false, 3>(a, warps_per_block, num_sms, 0, s);
-        }
-        if (l8) {
-            if (a.cap == 256) return launch_walk_t<0, 6, false, false, 8, 256>(a, warps_per_block, num_sms, 0, s);
-            if (a.cap == 1024) return launch_walk_t<0, 6, false, false, 8, 1024>(a, warps_per_block, num_sms, 0, s);
-            return launch_walk_t<0, 6, false, false, 8>(a, warps_per_block, num_sms, 0, s);
-        }
+        if (spec && launch_specialised<0>(a, warps_per_block, num_sms, s, &se)) return se;
         return launch_walk_t<0, 6, false, false>(a, warps_per_block, num_sms, 0, s);
     }
-    MCMI_WALK_RARE(1)
+    if (global_tier)
+        return a.deg_stats ? launch_walk_t<1, 4, true, true>(a, warps_per_block, num_sms, max_warps, s)
+                           : launch_walk_t<1, 4, true, false>(a, warps_per_block, num_sms, max_warps, s);
+    if (a.deg_stats) return launch_walk_t<1, 6, false, true>(a, warps_per_block, num_sms, 0, s);
     if (mb == 5) return launch_walk_t<1, 5, false, false>(a, warps_per_block, num_sms, 0, s);
     if (mb == 4) return launch_walk_t<1, 4, false, false>(a, warps_per_block, num_sms, 0, s);
-    if (l2) {
-        if (a.cap == 32) return launch_walk_t<1, 6, false, false, 2, 32>(a, warps_per_block, num_sms, 0, s);
-        if (a.cap == 64) return launch_walk_t<1, 6, false, false, 2, 64>(a, warps_per_block, num_sms, 0, s);
-        if (a.cap == 256) return launch_walk_t<1, 6, false, false, 2, 256>(a, warps_per_block, num_sms, 0, s);
-        return launch_walk_t<1, 6, false, false, 2>(a, warps_per_block, num_sms, 0, s);
-    }
-    if (l4) {
-        if (a.cap == 256) return launch_walk_t<1, 6, false, false, 4, 256>(a, warps_per_block, num_sms, 0, s);
-        return launch_walk_t<1, 6, false, false, 4>(a, warps_per_block, num_sms, 0, s);
-    }
-    if (l3) {
-        if (a.cap == 256) return launch_walk_t<1, 6, false, false, 3, 256>(a, warps_per_block, num_sms, 0, s);
-        return launch_walk_t<1, 6, false, false, 3>(a, warps_per_block, num_sms, 0, s);
-    }
-    if (l8) {
-        if (a.cap == 256) return launch_walk_t<1, 6, false, false, 8, 256>(a, warps_per_block, num_sms, 0, s);
-        if (a.cap == 1024) return launch_walk_t<1, 6, false, false, 8, 1024>(a, warps_per_block, num_sms, 0, s);
-        return launch_walk_t<1, 6, false, false, 8>(a, warps_per_block, num_sms, 0, s);
-    }
+    if (spec && launch_specialised<1>(a, warps_per_block, num_sms, s, &se)) return se;
     return launch_walk_t<1, 6, false, false>(a, warps_per_block, num_sms, 0, s);
-#undef MCMI_WALK_RARE
 }
 
 }  // namespace mcmi
