@@ -96,16 +96,104 @@ __global__ void k_sub(const double* __restrict__ a, const double* __restrict__ b
         r[i] = a[i] - b[i];
 }
 
-// p = r + beta * (p - omega * v)   (solvers.cpp:198-199)
-__global__ void k_bicg_p(const double* __restrict__ r, double beta, double omega, const double* __restrict__ v,
-                         double* __restrict__ p, int64_t n) {
+__global__ void k_fill(double* __restrict__ y, double v, int64_t n) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        y[i] = v;
+}
+
+// ---- BiCGstab with its scalars on the device: one host round trip per
+// iteration instead of five.  The scalar recurrences are the reference's
+// (solvers.cpp:184-238) evaluated by every thread from device memory, so they
+// round identically; the vector updates are fused but keep each element's
+// sequence of operations.
+struct BiState {
+    double rho, alpha, omega;      // carried across iterations
+    double rho1, r0v, tt, ts, rr;  // this iteration's dot products
+    int flag;                      // breakdown (rho1 or r0v below 1e-30) in this iteration
+    int pad;
+};
+
+// two dot products in one pass (same per-dot reduction order as k_dot_partial)
+__global__ void k_dot2_partial(const double* __restrict__ a1, const double* __restrict__ b1,
+                               const double* __restrict__ a2, const double* __restrict__ b2, int64_t n,
+                               double* __restrict__ partial1, double* __restrict__ partial2) {
+    __shared__ double red1[ST / 32], red2[ST / 32];
+    double s1 = 0.0, s2 = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        s1 += a1[i] * b1[i];
+        s2 += a2[i] * b2[i];
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+        s1 += __shfl_xor_sync(FULL_MASK, s1, o);
+        s2 += __shfl_xor_sync(FULL_MASK, s2, o);
+    }
+    if ((threadIdx.x & 31) == 0) {
+        red1[threadIdx.x >> 5] = s1;
+        red2[threadIdx.x >> 5] = s2;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t1 = 0.0, t2 = 0.0;
+        for (int w = 0; w < ST / 32; ++w) {
+            t1 += red1[w];
+            t2 += red2[w];
+        }
+        partial1[blockIdx.x] = t1;
+        partial2[blockIdx.x] = t2;
+    }
+}
+
+// p = r + beta * (p - omega * v), beta = (rho1 / rho) * (alpha / omega)   (solvers.cpp:190-199)
+__global__ void k_bicg_p_dev(BiState* st, const double* __restrict__ r, const double* __restrict__ v,
+                             double* __restrict__ p, int64_t n) {
+    const double rho1 = st->rho1;
+    if (fabs(rho1) < 1e-30) {  // breakdown: the reference stops before touching p
+        if (blockIdx.x == 0 && threadIdx.x == 0) st->flag = 1;
+        return;
+    }
+    const double beta = (rho1 / st->rho) * (st->alpha / st->omega);
+    const double omega = st->omega;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
         p[i] = r[i] + beta * (p[i] - omega * v[i]);
 }
 
-__global__ void k_fill(double* __restrict__ y, double v, int64_t n) {
+// alpha = rho1 / r0v; s = r - alpha * v   (solvers.cpp:201-208)
+__global__ void k_bicg_s_dev(BiState* st, const double* __restrict__ r, const double* __restrict__ v,
+                             double* __restrict__ sv, int64_t n) {
+    if (*reinterpret_cast<volatile int*>(&st->flag)) return;
+    const double r0v = st->r0v;
+    if (fabs(r0v) < 1e-30) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) st->flag = 1;
+        return;
+    }
+    const double alpha = st->rho1 / r0v;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-        y[i] = v;
+        sv[i] = r[i] + (-alpha) * v[i];
+}
+
+// omega = tt > 0 ? ts / tt : 0; x = (x + alpha p) + omega s; r = s - omega t   (solvers.cpp:210-220)
+__global__ void k_bicg_xr_dev(BiState* st, const double* __restrict__ p, const double* __restrict__ sv,
+                              const double* __restrict__ t, double* __restrict__ x, double* __restrict__ r,
+                              int64_t n) {
+    if (*reinterpret_cast<volatile int*>(&st->flag)) return;
+    const double alpha = st->rho1 / st->r0v;
+    const double tt = st->tt;
+    const double omega = tt > 0.0 ? st->ts / tt : 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        x[i] = (x[i] + alpha * p[i]) + omega * sv[i];
+        r[i] = sv[i] + (-omega) * t[i];
+    }
+}
+
+// carries alpha, omega, rho to the next iteration (after every block of k_bicg_xr_dev read them)
+__global__ void k_bicg_carry(BiState* st) {
+    if (st->flag) return;
+    const double alpha = st->rho1 / st->r0v;
+    const double tt = st->tt;
+    st->omega = tt > 0.0 ? st->ts / tt : 0.0;
+    st->alpha = alpha;
+    st->rho = st->rho1;
 }
 
 inline unsigned grid_n(int64_t n) {
@@ -151,6 +239,17 @@ struct Ctx {
         return *h_scal;
     }
     double norm2(const double* a) { return std::sqrt(dot(a, a)); }
+    // dot products into device slots, no host round trip
+    void dot_to(const double* a, const double* bb, double* out) {
+        k_dot_partial<<<kDotBlocks, ST, 0, s>>>(a, bb, n, partial);
+        k_dot_final<<<1, ST, 0, s>>>(partial, kDotBlocks, out);
+    }
+    void dot2_to(const double* a1, const double* b1, double* out1, const double* a2, const double* b2,
+                 double* out2) {
+        k_dot2_partial<<<kDotBlocks, ST, 0, s>>>(a1, b1, a2, b2, n, partial, partial + kDotBlocks);
+        k_dot_final<<<1, ST, 0, s>>>(partial, kDotBlocks, out1);
+        k_dot_final<<<1, ST, 0, s>>>(partial + kDotBlocks, kDotBlocks, out2);
+    }
     void axpy(double a, const double* x, double* y) { k_axpy<<<grid_n(n), ST, 0, s>>>(a, x, y, n); }
     void copy(double* dst, const double* src) {
         cudaMemcpyAsync(dst, src, static_cast<size_t>(n) * sizeof(double), cudaMemcpyDeviceToDevice, s);
@@ -284,40 +383,48 @@ int bicgstab(Ctx& c, const double* rhs, double* x, const mcmi_solver_config& cfg
     c.copy(r0, r);
     k_fill<<<grid_n(n), ST, 0, c.s>>>(p, 0.0, n);
     k_fill<<<grid_n(n), ST, 0, c.s>>>(vv, 0.0, n);
-    double rho = 1.0, alpha = 1.0, omega = 1.0;
+    BiState* st = nullptr;
+    BiState* h_st = nullptr;
+    if (c.err == cudaSuccess) c.err = cudaMallocAsync(&st, sizeof(BiState), c.s);
+    if (c.err == cudaSuccess) c.err = cudaMallocHost(&h_st, sizeof(BiState));
+    if (c.err != cudaSuccess) return MCMI_ENOMEM;
+    BiState init{};
+    init.rho = init.alpha = init.omega = 1.0;
+    *h_st = init;
+    cudaMemcpyAsync(st, h_st, sizeof(BiState), cudaMemcpyHostToDevice, c.s);
+    c.dot_to(r0, r, &st->rho1);
     while (rep.iterations < cfg.max_iters) {
-        const double rho1 = c.dot(r0, r);
-        if (std::abs(rho1) < 1e-30) {
-            rep.breakdown = 1;
-            break;
-        }
-        const double beta = (rho1 / rho) * (alpha / omega);
-        k_bicg_p<<<grid_n(n), ST, 0, c.s>>>(r, beta, omega, vv, p, n);
+        k_bicg_p_dev<<<grid_n(n), ST, 0, c.s>>>(st, r, vv, p, n);
         c.op(p, vv, tmp);
-        const double r0v = c.dot(r0, vv);
-        if (std::abs(r0v) < 1e-30) {
+        c.dot_to(r0, vv, &st->r0v);
+        k_bicg_s_dev<<<grid_n(n), ST, 0, c.s>>>(st, r, vv, s, n);
+        c.op(s, t, tmp);
+        c.dot2_to(t, t, &st->tt, t, s, &st->ts);
+        k_bicg_xr_dev<<<grid_n(n), ST, 0, c.s>>>(st, p, s, t, x, r, n);
+        k_bicg_carry<<<1, 1, 0, c.s>>>(st);
+        // ||r||^2 for the convergence test and the next iteration's rho1 = (r0, r)
+        c.dot2_to(r, r, &st->rr, r0, r, &st->rho1);
+        cudaMemcpyAsync(h_st, st, sizeof(BiState), cudaMemcpyDeviceToHost, c.s);
+        const cudaError_t e = cudaStreamSynchronize(c.s);
+        if (e != cudaSuccess) {
+            c.err = e;
+            break;
+        }
+        if (h_st->flag) {  // rho1 or r0v breakdown: the reference stops before the update
             rep.breakdown = 1;
             break;
         }
-        alpha = rho1 / r0v;
-        c.copy(s, r);
-        c.axpy(-alpha, vv, s);
-        c.op(s, t, tmp);
-        const double tt = c.dot(t, t);
-        omega = tt > 0.0 ? c.dot(t, s) / tt : 0.0;
-        c.axpy(alpha, p, x);
-        c.axpy(omega, s, x);
-        c.copy(r, s);
-        c.axpy(-omega, t, r);
-        rho = rho1;
         ++rep.iterations;
-        const double rel = c.norm2(r) / b_prec_norm;
+        const double rel = std::sqrt(h_st->rr) / b_prec_norm;
         if (rel <= cfg.rel_tol && c.true_rel(rhs, x, rhs_norm, tmp, tmp2) <= cfg.rel_tol) break;
-        if (omega == 0.0) {
+        if (h_st->omega == 0.0) {
             rep.breakdown = 1;
             break;
         }
     }
+    cudaFreeAsync(st, c.s);
+    cudaStreamSynchronize(c.s);
+    cudaFreeHost(h_st);
     rep.final_rel_residual = c.true_rel(rhs, x, rhs_norm, tmp, tmp2);
     rep.converged = rep.final_rel_residual <= cfg.rel_tol;
     return c.err == cudaSuccess ? MCMI_OK : MCMI_ECUDA;
@@ -346,7 +453,7 @@ int solve_device(const mcmi_csr_view& b, const mcmi_csr_view* m, const double* r
     c.b = DevCsr{b.n, b.row_ptr, b.col_idx, b.values};
     c.prec = m != nullptr;
     if (m) c.m = DevCsr{m->n, m->row_ptr, m->col_idx, m->values};
-    cudaMallocAsync(&c.partial, kDotBlocks * sizeof(double), s);
+    cudaMallocAsync(&c.partial, 2 * kDotBlocks * sizeof(double), s);
     cudaMallocAsync(&c.scal, sizeof(double), s);
     cudaMallocHost(&c.h_scal, sizeof(double));
     const double* rhs = rhs_in;
