@@ -13,6 +13,7 @@
 // at the rounding level and iteration counts agree within a small delta
 // (tests/test_gpu_solver.py states it).
 #include <cmath>
+#include <cstdint>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -32,6 +33,7 @@ struct DevCsr {
     const int64_t* rp;
     const int64_t* ci;
     const double* v;
+    const int* ci32;  // int32 copy of ci (n < 2^31): half the index traffic of every SpMV
 };
 
 // y = m * x (csr.cpp:159-170): one thread per row, sequential in stored order.
@@ -39,9 +41,18 @@ __global__ void k_spmv(DevCsr m, const double* __restrict__ x, double* __restric
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m.n;
          i += (int64_t)gridDim.x * blockDim.x) {
         double s = 0.0;
-        for (int64_t k = m.rp[i]; k < m.rp[i + 1]; ++k) s += m.v[k] * x[m.ci[k]];
+        const int64_t a = m.rp[i], b = m.rp[i + 1];
+        if (m.ci32)
+            for (int64_t k = a; k < b; ++k) s += m.v[k] * x[m.ci32[k]];
+        else
+            for (int64_t k = a; k < b; ++k) s += m.v[k] * x[m.ci[k]];
         y[i] = s;
     }
+}
+
+__global__ void k_cols32(const int64_t* __restrict__ ci, int64_t nnz, int* __restrict__ out) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x)
+        out[k] = static_cast<int>(ci[k]);
 }
 
 // partial[b] = sum over the block's grid-stride slice of a[i]*b[i]
@@ -62,8 +73,15 @@ __global__ void k_dot_partial(const double* __restrict__ a, const double* __rest
     }
 }
 
-__global__ void k_dot_final(const double* __restrict__ partial, int nb, double* __restrict__ out) {
+// block b sums partial + b * nb into out[b] (b = 0 only for a single dot;
+// out1 for block 1 of a paired dot)
+__global__ void k_dot_final(const double* __restrict__ partial, int nb, double* __restrict__ out,
+                            double* __restrict__ out1 = nullptr) {
     __shared__ double red[ST / 32];
+    if (blockIdx.x == 1) {
+        partial += nb;
+        out = out1;
+    }
     double s = 0.0;
     for (int i = threadIdx.x; i < nb; i += blockDim.x) s += partial[i];
 #pragma unroll
@@ -247,8 +265,7 @@ struct Ctx {
     void dot2_to(const double* a1, const double* b1, double* out1, const double* a2, const double* b2,
                  double* out2) {
         k_dot2_partial<<<kDotBlocks, ST, 0, s>>>(a1, b1, a2, b2, n, partial, partial + kDotBlocks);
-        k_dot_final<<<1, ST, 0, s>>>(partial, kDotBlocks, out1);
-        k_dot_final<<<1, ST, 0, s>>>(partial + kDotBlocks, kDotBlocks, out2);
+        k_dot_final<<<2, ST, 0, s>>>(partial, kDotBlocks, out1, out2);
     }
     void axpy(double a, const double* x, double* y) { k_axpy<<<grid_n(n), ST, 0, s>>>(a, x, y, n); }
     void copy(double* dst, const double* src) {
@@ -450,9 +467,24 @@ int solve_device(const mcmi_csr_view& b, const mcmi_csr_view* m, const double* r
     Ctx c;
     c.s = s;
     c.n = b.n;
-    c.b = DevCsr{b.n, b.row_ptr, b.col_idx, b.values};
+    c.b = DevCsr{b.n, b.row_ptr, b.col_idx, b.values, nullptr};
     c.prec = m != nullptr;
-    if (m) c.m = DevCsr{m->n, m->row_ptr, m->col_idx, m->values};
+    if (m) c.m = DevCsr{m->n, m->row_ptr, m->col_idx, m->values, nullptr};
+    // int32 column copies for the SpMVs (one pass each, reused every iteration)
+    int* ci32[2] = {nullptr, nullptr};
+    if (b.n > 0 && b.n < INT32_MAX) {
+        DevCsr* mats[2] = {&c.b, m ? &c.m : nullptr};
+        for (int q = 0; q < 2; ++q) {
+            if (!mats[q]) continue;
+            int64_t nnz = 0;
+            cudaMemcpyAsync(&nnz, mats[q]->rp + mats[q]->n, sizeof(int64_t), cudaMemcpyDeviceToHost, s);
+            cudaStreamSynchronize(s);
+            if (nnz > 0 && cudaMallocAsync(&ci32[q], nnz * sizeof(int), s) == cudaSuccess) {
+                k_cols32<<<grid_n(nnz), ST, 0, s>>>(mats[q]->ci, nnz, ci32[q]);
+                mats[q]->ci32 = ci32[q];
+            }
+        }
+    }
     cudaMallocAsync(&c.partial, 2 * kDotBlocks * sizeof(double), s);
     cudaMallocAsync(&c.scal, sizeof(double), s);
     cudaMallocHost(&c.h_scal, sizeof(double));
@@ -467,6 +499,8 @@ int solve_device(const mcmi_csr_view& b, const mcmi_csr_view* m, const double* r
     }
     const int code = cfg.method == 0 ? gmres(c, rhs, x, cfg, *rep, msg) : bicgstab(c, rhs, x, cfg, *rep, msg);
     c.release();
+    for (int* p : ci32)
+        if (p) cudaFreeAsync(p, s);
     cudaFreeAsync(c.partial, s);
     cudaFreeAsync(c.scal, s);
     cudaEventRecord(e1, s);
