@@ -95,6 +95,66 @@ __global__ void k_dot_final(const double* __restrict__ partial, int nb, double* 
     }
 }
 
+// k_dot_final's sum of nb partials, computed by every block of a kernel in
+// the same order (so each block holds the same value); returned to all threads
+__device__ __forceinline__ double block_sum_partials(const double* __restrict__ partial, int nb) {
+    __shared__ double red[ST / 32];
+    __shared__ double total;
+    double s = 0.0;
+    for (int i = threadIdx.x; i < nb; i += blockDim.x) s += partial[i];
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL_MASK, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < ST / 32; ++w) t += red[w];
+        total = t;
+    }
+    __syncthreads();
+    return total;
+}
+
+// Modified Gram-Schmidt step on device (solvers.cpp:81-86): h_i = sum of the
+// previous dot's partials (stored to hslot by block 0), w -= h_i * v (the
+// reference's axpy with -h_i), fused with the partial sums of the next dot
+// (w, u) in k_dot_partial's order (same grid, same per-thread slices), so
+// every value equals the separate dot / axpy / dot sequence.
+__global__ void k_mgs_step(const double* __restrict__ prev, double* __restrict__ hslot, const double* __restrict__ v,
+                           double* w, const double* u, int64_t n,  // u may alias w
+                           double* __restrict__ partial) {
+    __shared__ double red[ST / 32];
+    const double h = block_sum_partials(prev, kDotBlocks);
+    if (blockIdx.x == 0 && threadIdx.x == 0) *hslot = h;
+    const double a = -h;
+    double s = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double wi = w[i] + a * v[i];
+        w[i] = wi;
+        s += wi * (u == w ? wi : u[i]);
+    }
+#pragma unroll
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(FULL_MASK, s, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int ww = 0; ww < ST / 32; ++ww) t += red[ww];
+        partial[blockIdx.x] = t;
+    }
+}
+
+// h = sqrt((w, w)) from its partials (block 0 stores it), then v = w / h
+// unless h < 1e-14 (the lucky-breakdown test, solvers.cpp:87-89)
+__global__ void k_mgs_norm_div(const double* __restrict__ prev, double* __restrict__ hslot,
+                               const double* __restrict__ w, double* __restrict__ v, int64_t n) {
+    const double d = sqrt(block_sum_partials(prev, kDotBlocks));  // correctly rounded, like std::sqrt
+    if (blockIdx.x == 0 && threadIdx.x == 0) *hslot = d;
+    if (d < 1e-14) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+        v[i] = w[i] / d;
+}
+
 // y += a * x  (solvers.cpp:19-21)
 __global__ void k_axpy(double a, const double* __restrict__ x, double* __restrict__ y, int64_t n) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -302,7 +362,20 @@ int gmres(Ctx& c, const double* rhs, double* x, const mcmi_solver_config& cfg, m
     std::vector<double*> v(static_cast<size_t>(restart + 1), nullptr);
     for (auto& p : v) p = c.vec();
     double* w = c.vec();
+    double* hcol = nullptr;   // column j of H on the device
+    double* h_hcol = nullptr;
+    if (c.err == cudaSuccess) c.err = cudaMallocAsync(&hcol, (restart + 2) * sizeof(double), c.s);
+    if (c.err == cudaSuccess) c.err = cudaMallocHost(&h_hcol, (restart + 2) * sizeof(double));
     if (c.err != cudaSuccess) return MCMI_ENOMEM;
+    struct Free {
+        double *d, *hh;
+        cudaStream_t s;
+        ~Free() {
+            cudaFreeAsync(d, s);
+            cudaStreamSynchronize(s);
+            cudaFreeHost(hh);
+        }
+    } free_h{hcol, h_hcol, c.s};
     std::vector<std::vector<double>> h(restart + 1, std::vector<double>(restart, 0.0));
     std::vector<double> cs(restart), sn(restart), g(restart + 1);
     bool done = false;
@@ -321,13 +394,24 @@ int gmres(Ctx& c, const double* rhs, double* x, const mcmi_solver_config& cfg, m
         bool cycle_end = false;
         while (j < restart && !cycle_end) {
             c.op(v[j], w, tmp);
-            for (int64_t i = 0; i <= j; ++i) {  // modified Gram-Schmidt
-                h[i][j] = c.dot(w, v[i]);
-                c.axpy(-h[i][j], v[i], w);
+            // modified Gram-Schmidt with h on the device: j + 3 launches and one
+            // host round trip per iteration (same dots, same axpys)
+            double* pa = c.partial;
+            double* pb = c.partial + kDotBlocks;
+            k_dot_partial<<<kDotBlocks, ST, 0, c.s>>>(w, v[0], n, pa);
+            for (int64_t i = 0; i <= j; ++i) {
+                const double* u = i < j ? v[i + 1] : w;  // next dot: (w, v_{i+1}), or (w, w) for the norm
+                k_mgs_step<<<kDotBlocks, ST, 0, c.s>>>(pa, hcol + i, v[i], w, u, n, pb);
+                std::swap(pa, pb);
             }
-            h[j + 1][j] = c.norm2(w);
+            k_mgs_norm_div<<<kDotBlocks, ST, 0, c.s>>>(pa, hcol + j + 1, w, v[j + 1], n);
+            cudaMemcpyAsync(h_hcol, hcol, (j + 2) * sizeof(double), cudaMemcpyDeviceToHost, c.s);
+            if (const cudaError_t e = cudaStreamSynchronize(c.s); e != cudaSuccess) {
+                c.err = e;
+                break;
+            }
+            for (int64_t i = 0; i <= j + 1; ++i) h[i][j] = h_hcol[i];
             const bool lucky = h[j + 1][j] < 1e-14;
-            if (!lucky) k_div<<<grid_n(n), ST, 0, c.s>>>(w, h[j + 1][j], v[j + 1], n);
             for (int64_t i = 0; i < j; ++i) {
                 const double t = cs[i] * h[i][j] + sn[i] * h[i + 1][j];
                 h[i + 1][j] = -sn[i] * h[i][j] + cs[i] * h[i + 1][j];
