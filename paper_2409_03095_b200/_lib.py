@@ -113,7 +113,7 @@ def load(path: str | None = None):
     path = path or os.environ.get("MCMI_LIB_PATH") or LIB
     if not os.path.exists(path):
         raise ImportError(
-            f"{path} not found: the CUDA library is required (run `python -m paper_2409_03095_b200.build`)")
+            f"{path} not found: the CUDA library is required (run `python paper_2409_03095_b200/build.py` or `python __graft_entry__.py`)")
     L = C.CDLL(path)
     L.mcmi_config_default.argtypes = [C.POINTER(mcmi_config)]
     L.mcmi_config_default.restype = None
