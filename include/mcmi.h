@@ -76,7 +76,9 @@ typedef struct mcmi_config {
     int32_t rng_mode; /* MCMI_RNG_*, default MCMI_RNG_REFERENCE */
     int32_t device;   /* CUDA device ordinal for mcmi_build */
     int32_t flags;    /* MCMI_FLAG_*, default 0 */
-    int32_t reserved;
+    int32_t n_gpus;   /* host builds (mcmi_build*): row blocks on devices device..device+n_gpus-1,
+                         one host thread each; 0 = env MCMI_GPUS (default 1).  M does not
+                         depend on it.  The device-resident engine ignores it. */
 } mcmi_config;
 
 /* flags */

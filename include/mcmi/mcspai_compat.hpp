@@ -47,6 +47,7 @@ namespace compat {
 struct Options {
     int device = 0;                      // CUDA device ordinal
     int rng_mode = MCMI_RNG_REFERENCE;   // byte-identical to the reference by default
+    int n_gpus = 0;                      // row blocks on devices device..device+n_gpus-1; 0 = env MCMI_GPUS or 1
 };
 
 template <class CfgT>
@@ -67,6 +68,7 @@ mcmi_config to_config(const CfgT& cfg, const Options& opt) {
     c.master_seed = cfg.master_seed;
     c.rng_mode = opt.rng_mode;
     c.device = opt.device;
+    c.n_gpus = opt.n_gpus;
     return c;
 }
 

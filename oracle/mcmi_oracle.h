@@ -38,7 +38,7 @@ typedef struct orc_config {
     int32_t rng_mode; /* 0 reference stream, 1 keyed (row, chain, step) */
     int32_t device;   /* ignored */
     int32_t flags;    /* ignored (the oracle always counts) */
-    int32_t reserved;
+    int32_t n_gpus;   /* ignored */
 } orc_config;
 
 typedef struct orc_result orc_result;

@@ -35,7 +35,7 @@ class OrcConfig(C.Structure):
         ("rng_mode", C.c_int32),
         ("device", C.c_int32),
         ("flags", C.c_int32),
-        ("reserved", C.c_int32),
+        ("n_gpus", C.c_int32),
     ]
 
 
@@ -73,7 +73,7 @@ def lib():
 def make_config(**kw) -> OrcConfig:
     c = OrcConfig(epsilon=0.0625, delta=0.0625, alpha=5.0, mode=1, drop_mode=0, drop_fraction=0.0,
                   retain_k=0, has_chains_override=0, has_max_len_override=0, chains_override=0,
-                  max_len_override=0, master_seed=0, rng_mode=0, device=0, flags=0, reserved=0)
+                  max_len_override=0, master_seed=0, rng_mode=0, device=0, flags=0, n_gpus=0)
     for k, v in kw.items():
         if k == "chains_override":
             if v is not None:

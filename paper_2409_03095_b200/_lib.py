@@ -44,7 +44,7 @@ class mcmi_config(C.Structure):
         ("rng_mode", C.c_int32),
         ("device", C.c_int32),
         ("flags", C.c_int32),
-        ("reserved", C.c_int32),
+        ("n_gpus", C.c_int32),
     ]
 
 

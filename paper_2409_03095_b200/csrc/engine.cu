@@ -14,6 +14,7 @@
 #include <cstring>
 #include <mutex>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "mcmi.h"
@@ -821,21 +822,210 @@ Status build_from_host(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config
 
 }  // namespace
 
-struct mcmi_result {
-    int device = 0;
-    int64_t n = 0, nnz = 0;
-    int64_t n_chains = 1, max_len = 1;
-    mcmi_stats stats{};
-    // The result keeps its engine checked out of the cache: the arrays below
-    // are the engine's own buffers (no per-call device allocation or free);
-    // mcmi_result_free returns the engine to the cache.
+// One device shard of a host build: the arrays are the engine's own output
+// buffers (no per-call device allocation or free); the result keeps the engine
+// checked out of the cache until mcmi_result_free.
+struct ResultPart {
     mcmi_engine* engine = nullptr;
+    int64_t rows = 0, nnz = 0;
     const int64_t* rp = nullptr;
     const int64_t* ci = nullptr;
     const double* v = nullptr;
     const int64_t* cu = nullptr;
     const int64_t* eb = nullptr;
 };
+
+struct mcmi_result {
+    int64_t n = 0, nnz = 0;
+    int64_t n_chains = 1, max_len = 1;
+    mcmi_stats stats{};
+    std::vector<ResultPart> parts;  // row blocks in row order (one per GPU)
+};
+
+namespace {
+
+// Devices of a build: cfg.n_gpus (0 = env MCMI_GPUS, else 1) consecutive
+// ordinals from cfg.device.  MCMI_SHARD_WRAP=1 maps ordinals modulo the
+// visible device count (several shards per GPU: a test hook for one-GPU boxes).
+Status shard_devices(const mcmi_config& cfg, std::vector<int>* devs) {
+    int g = cfg.n_gpus;
+    if (g <= 0) {
+        const char* env = std::getenv("MCMI_GPUS");
+        g = env && *env ? std::atoi(env) : 1;
+        if (g <= 0) g = 1;
+    }
+    devs->clear();
+    if (g == 1) {
+        devs->push_back(cfg.device);
+        return ok();
+    }
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count <= 0) {
+        cudaGetLastError();
+        return fail(MCMI_ENODEV, "no CUDA device");
+    }
+    const char* wrap = std::getenv("MCMI_SHARD_WRAP");
+    const bool wrapped = wrap && *wrap && std::strcmp(wrap, "0") != 0;
+    for (int i = 0; i < g; ++i) {
+        const int d = cfg.device + i;
+        if (d >= count && !wrapped)
+            return fail(MCMI_ENODEV, "n_gpus=" + std::to_string(g) + " needs devices " + std::to_string(cfg.device) +
+                                         ".." + std::to_string(cfg.device + g - 1) + " but " +
+                                         std::to_string(count) + " are visible");
+        devs->push_back(d % count);
+    }
+    return ok();
+}
+
+// Contiguous row blocks of [lo, hi) balanced on cost(r) = 1 + nnz(r): block g
+// starts at the first row whose cost prefix reaches total * g / G (the same
+// edges as distributed.partition_rows).
+std::vector<int64_t> partition_rows(const int64_t* rp, int64_t lo, int64_t hi, int g) {
+    std::vector<int64_t> edges(static_cast<size_t>(g) + 1, lo);
+    edges[g] = hi;
+    if (hi <= lo) return edges;
+    auto cost = [&](int64_t i) { return static_cast<double>(i - lo) + static_cast<double>(rp[i] - rp[lo]); };
+    const double total = cost(hi);
+    for (int k = 1; k < g; ++k) {
+        const double target = total * k / g;
+        int64_t a = lo, b = hi + 1;  // first i in [lo, hi] with cost(i) >= target
+        while (a < b) {
+            const int64_t m = a + (b - a) / 2;
+            if (cost(m) < target) a = m + 1;
+            else b = m;
+        }
+        edges[k] = std::max(std::min(a, hi), edges[k - 1]);
+    }
+    return edges;
+}
+
+// Builds rows [lo, hi) on every device of the build, one host thread per
+// shard (each stages B on its own GPU); rows are independent
+// (mc_engine.cpp:164-178), so the row-ordered concatenation of the shards is
+// the single-GPU M.  On success the result owns the engines.
+Status build_parts(const mcmi_csr_view& b, const mcmi_config& cfg, int64_t lo, int64_t hi, mcmi_result* r) {
+    std::vector<int> devs;
+    if (Status st = shard_devices(cfg, &devs); st.code) return st;
+    const int64_t n = b.n;
+    if (lo < 0) lo = 0;
+    if (hi < 0 || hi > n) hi = n;
+    if (hi < lo) hi = lo;
+    const int g = static_cast<int>(devs.size());
+    if (g > 1 && n > 0 && !b.row_ptr) return fail(MCMI_EINVAL, "null row_ptr");
+    const std::vector<int64_t> edges = g > 1 ? partition_rows(b.row_ptr, lo, hi, g) : std::vector<int64_t>{lo, hi};
+    struct Job {
+        mcmi_engine* e = nullptr;
+        mcmi_device_csr dc{};
+        mcmi_stats st{};
+        Status status;
+    };
+    std::vector<Job> jobs(static_cast<size_t>(g));
+    auto run = [&](int i) {
+        Job& j = jobs[static_cast<size_t>(i)];
+        j.e = acquire_engine(devs[static_cast<size_t>(i)], &j.status);
+        if (!j.e) return;
+        mcmi_config c = cfg;
+        c.device = devs[static_cast<size_t>(i)];
+        j.status = build_from_host(j.e, b, c, edges[i], edges[i + 1], &j.dc, &j.st, nullptr);
+    };
+    if (g == 1) {
+        run(0);
+    } else {
+        std::vector<std::thread> threads;
+        for (int i = 0; i < g; ++i) threads.emplace_back(run, i);
+        for (auto& t : threads) t.join();
+    }
+    Status first;
+    for (auto& j : jobs)
+        if (j.status.code && !first.code) first = j.status;
+    if (first.code) {
+        for (auto& j : jobs)
+            if (j.e) release_engine(j.e);
+        return first;
+    }
+    r->n = hi - lo;
+    r->nnz = 0;
+    mcmi_stats& t = r->stats;
+    t = jobs[0].st;
+    for (size_t i = 0; i < jobs.size(); ++i) {
+        const Job& j = jobs[i];
+        ResultPart p;
+        p.engine = j.e;
+        p.rows = j.dc.row_end - j.dc.row_begin;
+        p.nnz = j.dc.nnz;
+        p.rp = j.dc.row_ptr;
+        p.ci = j.dc.col_idx;
+        p.v = j.dc.values;
+        p.cu = j.dc.chains_used;
+        p.eb = j.dc.entries_before;
+        r->parts.push_back(p);
+        r->nnz += p.nnz;
+        if (i == 0) continue;
+        t.rows += j.st.rows;
+        t.nnz += j.st.nnz;
+        t.walk_steps += j.st.walk_steps;
+        if (t.walk_deg_sum >= 0 && j.st.walk_deg_sum >= 0) t.walk_deg_sum += j.st.walk_deg_sum;
+        t.rows_retried += j.st.rows_retried;
+        t.launches += j.st.launches;
+        t.hash_cap = std::max(t.hash_cap, j.st.hash_cap);
+        // device times: the shards run concurrently, the build takes the slowest
+        t.ms_tables = std::max(t.ms_tables, j.st.ms_tables);
+        t.ms_walk = std::max(t.ms_walk, j.st.ms_walk);
+        t.ms_assemble = std::max(t.ms_assemble, j.st.ms_assemble);
+        t.ms_total = std::max(t.ms_total, j.st.ms_total);
+        t.ms_walk_kernel = std::max(t.ms_walk_kernel, j.st.ms_walk_kernel);
+    }
+    r->n_chains = t.n_chains;
+    r->max_len = t.max_len;
+    return ok();
+}
+
+// Copies the parts to their global offsets in the caller's arrays (any pointer
+// may be NULL): every GPU's device->host copy is in flight at once, then the
+// shard-local row pointers are shifted by the entries of the shards before.
+int copy_parts(const mcmi_result* r, int64_t* row_ptr, int64_t* col_idx, double* values, int64_t* chains_used,
+               int64_t* entries_before) {
+    cudaError_t e = cudaSuccess;
+    int64_t row_off = 0, nnz_off = 0;
+    for (const ResultPart& p : r->parts) {
+        if (e == cudaSuccess) e = cudaSetDevice(p.engine->device);
+        cudaStream_t s = p.engine->own;
+        auto cp = [&](void* dst, const void* src, size_t bytes) {
+            if (dst && src && bytes && e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s);
+        };
+        cp(col_idx ? col_idx + nnz_off : nullptr, p.ci, p.nnz * sizeof(int64_t));  // largest first
+        cp(values ? values + nnz_off : nullptr, p.v, p.nnz * sizeof(double));
+        cp(row_ptr ? row_ptr + row_off : nullptr, p.rp, p.rows * sizeof(int64_t));  // row_ptr[n] is set below
+        cp(chains_used ? chains_used + row_off : nullptr, p.cu, p.rows * sizeof(int64_t));
+        cp(entries_before ? entries_before + row_off : nullptr, p.eb, p.rows * sizeof(int64_t));
+        row_off += p.rows;
+        nnz_off += p.nnz;
+    }
+    for (const ResultPart& p : r->parts) {
+        if (e == cudaSuccess) e = cudaSetDevice(p.engine->device);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(p.engine->own);
+    }
+    if (e != cudaSuccess) return MCMI_ECUDA;
+    if (row_ptr) {
+        row_off = nnz_off = 0;
+        for (const ResultPart& p : r->parts) {
+            if (nnz_off)
+                for (int64_t i = 0; i < p.rows; ++i) row_ptr[row_off + i] += nnz_off;
+            row_off += p.rows;
+            nnz_off += p.nnz;
+        }
+        row_ptr[row_off] = nnz_off;
+    }
+    return MCMI_OK;
+}
+
+void free_parts(mcmi_result* r) {
+    for (ResultPart& p : r->parts)
+        if (p.engine) release_engine(p.engine);
+    r->parts.clear();
+}
+
+}  // namespace
 
 extern "C" {
 
@@ -887,29 +1077,12 @@ int mcmi_build_rows(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_
                     int64_t row_end, mcmi_result** out, char* err, size_t errlen) {
     *out = nullptr;
     if (!b || !cfg) return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
-    Status st;
-    mcmi_engine* e = acquire_engine(cfg->device, &st);
-    if (!e) return report(st, err, errlen);
-    mcmi_device_csr dc{};
-    mcmi_stats stats{};
-    st = build_from_host(e, *b, *cfg, row_begin, row_end, &dc, &stats, nullptr);
+    auto* r = new mcmi_result();
+    const Status st = build_parts(*b, *cfg, row_begin, row_end, r);
     if (st.code) {
-        release_engine(e);
+        delete r;
         return report(st, err, errlen);
     }
-    auto* r = new mcmi_result();  // owns the engine (and its output buffers) until freed
-    r->device = e->device;
-    r->n = dc.row_end - dc.row_begin;
-    r->nnz = dc.nnz;
-    r->n_chains = stats.n_chains;
-    r->max_len = stats.max_len;
-    r->stats = stats;
-    r->engine = e;
-    r->rp = dc.row_ptr;
-    r->ci = dc.col_idx;
-    r->v = dc.values;
-    r->cu = dc.chains_used;
-    r->eb = dc.entries_before;
     *out = r;
     return MCMI_OK;
 }
@@ -920,13 +1093,36 @@ int mcmi_build_into(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_
                     char* err, size_t errlen) {
     if (!b || !cfg || !row_ptr || !nnz || (capacity > 0 && (!col_idx || !values)))
         return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    std::vector<int> devs;
+    if (Status st = shard_devices(*cfg, &devs); st.code) return report(st, err, errlen);
+    if (devs.size() > 1) {
+        // several GPUs: shards are built concurrently, then each GPU copies its
+        // shard straight to its global offset (offsets are known only after
+        // every shard has its entry count, so the copies do not overlap the walks)
+        mcmi_result r;
+        Status st = build_parts(*b, *cfg, row_begin, row_end, &r);
+        if (st.code) return report(st, err, errlen);
+        *nnz = r.nnz;
+        if (stats) *stats = r.stats;
+        int code = MCMI_OK;
+        if (r.nnz > capacity) {
+            st = fail(MCMI_ENOMEM, "output capacity " + std::to_string(capacity) + " < nnz " + std::to_string(r.nnz));
+        } else {
+            code = copy_parts(&r, row_ptr, col_idx, values, chains_used, entries_before);
+            if (code) st = fail(code, "device->host copy failed");
+        }
+        free_parts(&r);
+        return report(st, err, errlen);
+    }
+    mcmi_config c = *cfg;
+    c.device = devs[0];
     Status st;
-    mcmi_engine* e = acquire_engine(cfg->device, &st);
+    mcmi_engine* e = acquire_engine(c.device, &st);
     if (!e) return report(st, err, errlen);
     const HostSink sink{row_ptr, col_idx, values, capacity, chains_used, entries_before};
     mcmi_device_csr dc{};
     mcmi_stats ls{};
-    st = build_from_host(e, *b, *cfg, row_begin, row_end, &dc, &ls, &sink);
+    st = build_from_host(e, *b, c, row_begin, row_end, &dc, &ls, &sink);
     *nnz = ls.nnz;
     if (stats) *stats = ls;
     release_engine(e);
@@ -944,21 +1140,10 @@ int mcmi_result_copy(const mcmi_result* r, int64_t* row_ptr, int64_t* col_idx, d
                      int64_t* chains_used, int64_t* entries_before, int64_t* n_chains,
                      int64_t* max_len) {
     if (!r) return MCMI_EINVAL;
-    if (cudaSetDevice(r->device) != cudaSuccess) return MCMI_ECUDA;
-    cudaStream_t s = r->engine->own;
-    cudaError_t e = cudaSuccess;
-    auto cp = [&](void* dst, const void* src, size_t bytes) {
-        if (dst && src && bytes && e == cudaSuccess) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s);
-    };
-    cp(col_idx, r->ci, r->nnz * sizeof(int64_t));  // largest first
-    cp(values, r->v, r->nnz * sizeof(double));
-    cp(row_ptr, r->rp, (r->n + 1) * sizeof(int64_t));
-    cp(chains_used, r->cu, r->n * sizeof(int64_t));
-    cp(entries_before, r->eb, r->n * sizeof(int64_t));
-    if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+    const int code = copy_parts(r, row_ptr, col_idx, values, chains_used, entries_before);
     if (n_chains) *n_chains = r->n_chains;
     if (max_len) *max_len = r->max_len;
-    return e == cudaSuccess ? MCMI_OK : MCMI_ECUDA;
+    return code;
 }
 
 int mcmi_result_stats(const mcmi_result* r, mcmi_stats* stats) {
@@ -969,7 +1154,7 @@ int mcmi_result_stats(const mcmi_result* r, mcmi_stats* stats) {
 
 void mcmi_result_free(mcmi_result* r) {
     if (!r) return;
-    if (r->engine) release_engine(r->engine);
+    free_parts(r);
     delete r;
 }
 

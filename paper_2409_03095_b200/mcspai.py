@@ -7,7 +7,7 @@ Same names, argument meaning and error behaviour as
 =========================  ===============================================
 reference (C++)            here
 =========================  ===============================================
-``McConfig``               :class:`McConfig` (+ ``rng_mode``, ``device``)
+``McConfig``               :class:`McConfig` (+ ``rng_mode``, ``device``, ``n_gpus``)
 ``CsrMatrix``              :class:`CsrMatrix` (int64 / float64 numpy)
 ``ApproxInverse``          :class:`ApproxInverse`
 ``RowMeta``                :class:`RowMeta` (column arrays)
@@ -19,8 +19,10 @@ reference (C++)            here
 =========================  ===============================================
 
 Every call goes through the C-ABI (include/mcmi.h) into the sm_100a kernels.
-``n_threads`` is accepted for signature compatibility; the device count of a
-sharded build is chosen by :mod:`paper_2409_03095_b200.distributed`.
+``n_threads`` is accepted for signature compatibility.  A host build uses
+``McConfig.n_gpus`` GPUs of this process (row blocks, one host thread per
+GPU); one process per GPU with device-resident shards is
+:mod:`paper_2409_03095_b200.distributed`.
 """
 from __future__ import annotations
 
@@ -77,6 +79,9 @@ class McConfig:  # mc_engine.hpp:15-26
     master_seed: int = 0
     rng_mode: RngMode = RngMode.reference
     device: int = 0
+    #: GPUs of a host build (row blocks on devices device..device+n_gpus-1, one
+    #: host thread each); 0 = env MCMI_GPUS, else 1.  M does not depend on it.
+    n_gpus: int = 0
     deg_stats: bool = False  #: also count sum deg(s) over steps (stats["walk_deg_sum"]); ~4% slower
 
     def to_c(self) -> L.mcmi_config:
@@ -95,6 +100,7 @@ class McConfig:  # mc_engine.hpp:15-26
         c.master_seed = int(self.master_seed) & 0xFFFFFFFFFFFFFFFF
         c.rng_mode = int(self.rng_mode)
         c.device = int(self.device)
+        c.n_gpus = int(self.n_gpus)
         c.flags = L.MCMI_FLAG_DEG_STATS if self.deg_stats else 0
         return c
 
