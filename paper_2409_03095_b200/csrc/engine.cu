@@ -6,6 +6,7 @@
 //   CSR assembly in row order                       (assemble.cu, device)
 // There is no CPU fallback: every failure to reach the device is an error.
 #include <algorithm>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdarg>
@@ -267,9 +268,9 @@ Tier make_tier(int cap, int64_t max_len) {
 }
 
 // Global-memory tier: any row size, full-width batches for long walks.
-Tier make_global_tier(int64_t bound, int64_t max_len) {
+Tier make_global_tier(int64_t bound, int64_t max_len, int64_t min_cap = 8192) {
     Tier t;
-    int64_t cap = 8192;
+    int64_t cap = min_cap;
     while (cap - cap / 4 < bound && cap < (int64_t{1} << 30)) cap <<= 1;
     t.cap = static_cast<int>(cap);
     t.cap_limit = t.cap - t.cap / 4;
@@ -425,13 +426,17 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     const int64_t deposits = sat_mul(N, std::max<int64_t>(L, 0));  // distinct <= 1 + N*L
     int64_t bound = std::min<int64_t>(n1, reach);
     if (deposits < INT64_MAX) bound = std::min<int64_t>(bound, deposits + 1);
-    static const int kTierCaps[] = {256, 1024};  // larger rows: the global tier (32 warps/SM)
+    // Tiers: shared-memory tables up to 256 slots (48 warps/SM), then a 1024-slot
+    // tier and the tier sized to the bound, both in global scratch (32 warps/SM).
+    // A 1024-slot table in shared memory fits 16 warps/SM, too few to cover the
+    // DRAM latency of the walks that need it (C5: 1.25x slower, profiles/
+    // r01_c5_l8_walk_summary.txt); from global scratch it is L2-resident.
     int first_cap = static_cast<int>(std::min<int64_t>(256, std::max<int64_t>(32, next_pow2((bound * 4 + 2) / 3))));
     std::vector<Tier> tiers;
     if (L <= kMaxSmemWalkLen) {
         tiers.push_back(make_tier(first_cap, L));
-        for (int c : kTierCaps)
-            if (c > first_cap && (tiers.back().cap_limit < bound)) tiers.push_back(make_tier(c, L));
+        if (first_cap < 256 && tiers.back().cap_limit < bound) tiers.push_back(make_tier(256, L));
+        if (tiers.back().cap_limit < bound) tiers.push_back(make_global_tier(0, L, 1024));
     }
     if (tiers.empty() || tiers.back().cap_limit < bound) tiers.push_back(make_global_tier(bound, L));
     st.hash_cap = first_cap;  // updated below if the pilot starts on a larger tier
@@ -456,6 +461,11 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     // the number of rows that overflowed it (listed in ovf[cur] on return).
     auto run_tier = [&](const Tier& t, int64_t work, const int* row_list, int64_t offset,
                         int64_t* overflowed) -> Status {
+        static const bool trace = getenv("MCMI_WALK_TRACE") != nullptr;
+        const auto h0 = std::chrono::steady_clock::now();
+        auto since = [&](std::chrono::steady_clock::time_point a) {
+            return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - a).count();
+        };
         const int64_t stride = stride_of(t);
         const int64_t need = pool_used + work * stride;
         MCMI_TRY(e->stage_col.grow_preserve(need * sizeof(int), pool_used * sizeof(int), s), "alloc staging");
@@ -505,6 +515,8 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         wa.entries_before = e->entries_before.as<int64_t>();
         wa.counters = e->counters.as<unsigned long long>();
         wa.overflow_list = e->ovf[cur].as<int>();
+        const double setup_ms = trace ? since(h0) : 0.0;
+        const auto h1 = std::chrono::steady_clock::now();
         MCMI_TRY(cudaEventRecord(e->ev[4], s), "cudaEventRecord");
         MCMI_TRY(launch_walk(wa, t.warps_per_block, e->num_sms, t.global, max_warps, s), "walk kernel");
         MCMI_TRY(cudaEventRecord(e->ev[5], s), "cudaEventRecord");
@@ -516,6 +528,9 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         float tw = 0;
         cudaEventElapsedTime(&tw, e->ev[4], e->ev[5]);
         st.ms_walk_kernel += tw;
+        if (trace)  // MCMI_WALK_TRACE=1: host setup / launch-to-sync wall / kernel device time per tier launch
+            std::fprintf(stderr, "mcmi walk: cap %d%s rows %lld setup %.2f ms wall %.2f ms kernel %.2f ms\n", t.cap,
+                         t.global ? " (global)" : "", static_cast<long long>(work), setup_ms, since(h1), tw);
         total_steps += e->h_ctr[1];
         total_deg += e->h_ctr[2];
         pool_used += work * stride;
@@ -546,9 +561,10 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         MCMI_TRY(cudaStreamSynchronize(s), "read pilot");
         // A row of s distinct columns costs c_t on the tier that holds it and
         // ~c_t * limit_t / s on each tier it overflows first (it aborts once the
-        // table is full).  Relative costs follow occupancy: smem <= 256: 1,
-        // smem 1024: 2, global: 3 (measured on the C5 grid, tools/c5_sweep.py).
-        auto tier_cost = [](const Tier& t) { return t.global ? 3.0 : (t.cap <= 256 ? 1.0 : 2.0); };
+        // table is full).  Relative costs (measured on the C5 grid,
+        // tools/c5_sweep.py): shared memory (<= 256 slots, 48 warps/SM) 1, the
+        // 1024-slot global-scratch tier 2, larger global tables 3.
+        auto tier_cost = [](const Tier& t) { return t.global ? (t.cap <= 1024 ? 2.0 : 3.0) : 1.0; };
         double best = 0.0;
         for (size_t c0 = 0; c0 < tiers.size(); ++c0) {
             double cost = 0.0;

@@ -981,9 +981,8 @@ bool launch_specialised(const WalkArgs& a, int wpb, int sms, cudaStream_t s, cud
                                 : launch_walk_t<MODE, 6, false, false, 4>(a, wpb, sms, 0, s);
             return true;
         case 8:
-            *err = a.cap == 256    ? launch_walk_t<MODE, 6, false, false, 8, 256>(a, wpb, sms, 0, s)
-                   : a.cap == 1024 ? launch_walk_t<MODE, 6, false, false, 8, 1024>(a, wpb, sms, 0, s)
-                                   : launch_walk_t<MODE, 6, false, false, 8>(a, wpb, sms, 0, s);
+            *err = a.cap == 256 ? launch_walk_t<MODE, 6, false, false, 8, 256>(a, wpb, sms, 0, s)
+                                : launch_walk_t<MODE, 6, false, false, 8>(a, wpb, sms, 0, s);
             return true;
         default:
             return false;
