@@ -142,6 +142,12 @@ int mcmi_build_into(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_
                     int64_t* row_ptr, int64_t* col_idx, double* values, int64_t capacity,
                     int64_t* chains_used, int64_t* entries_before, int64_t* nnz, mcmi_stats* stats,
                     char* err, size_t errlen);
+/* Row blocks of a sharded build: edges[0..parts] with block g =
+ * rows [edges[g], edges[g+1]) of [row_begin, row_end), balanced on cost(r) =
+ * 1 + nnz(r); edges[g] (0 < g < parts) is the first row whose cost prefix
+ * reaches total*g/parts.  Used by host builds with n_gpus > 1 and by the
+ * one-process-per-GPU driver (distributed.partition_rows).  Host only. */
+int mcmi_partition_rows(const int64_t* row_ptr, int64_t row_begin, int64_t row_end, int parts, int64_t* edges);
 int mcmi_result_sizes(const mcmi_result* r, int64_t* n, int64_t* nnz);
 /* Any pointer may be NULL.  row_ptr[n+1], col_idx[nnz], values[nnz],
  * chains_used[n] / entries_before[n] = RowMeta (mc_engine.hpp:33-36),

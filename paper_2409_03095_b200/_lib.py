@@ -18,7 +18,7 @@ _f64p = C.POINTER(C.c_double)
 
 #: every symbol include/mcmi.h declares
 EXPORTS = [
-    "mcmi_config_default", "mcmi_build", "mcmi_build_rows", "mcmi_build_into", "mcmi_result_sizes", "mcmi_result_copy",
+    "mcmi_config_default", "mcmi_build", "mcmi_build_rows", "mcmi_build_into", "mcmi_partition_rows", "mcmi_result_sizes", "mcmi_result_copy",
     "mcmi_result_stats", "mcmi_result_free", "mcmi_engine_create", "mcmi_engine_destroy",
     "mcmi_engine_build", "mcmi_copy", "mcmi_version", "mcmi_solver_config_default", "mcmi_solve_device",
     "mcmi_host_register", "mcmi_host_unregister", "mcmi_from_triplets", "mcmi_mm_parse", "mcmi_mm_read_file",
@@ -124,6 +124,7 @@ def load(path: str | None = None):
     L.mcmi_build_into.argtypes = [C.POINTER(mcmi_csr_view), C.POINTER(mcmi_config), C.c_int64, C.c_int64,
                                   C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p,
                                   C.POINTER(C.c_int64), C.POINTER(mcmi_stats), C.c_char_p, C.c_size_t]
+    L.mcmi_partition_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     L.mcmi_result_sizes.argtypes = [C.c_void_p, _i64p, _i64p]
     L.mcmi_result_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    _i64p, _i64p]

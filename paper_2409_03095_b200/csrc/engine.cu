@@ -1145,6 +1145,13 @@ int mcmi_build_into(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_
     return report(st, err, errlen);
 }
 
+int mcmi_partition_rows(const int64_t* row_ptr, int64_t row_begin, int64_t row_end, int parts, int64_t* edges) {
+    if (!row_ptr || !edges || parts < 1 || row_begin < 0 || row_end < row_begin) return MCMI_EINVAL;
+    const std::vector<int64_t> e = partition_rows(row_ptr, row_begin, row_end, parts);
+    std::copy(e.begin(), e.end(), edges);
+    return MCMI_OK;
+}
+
 int mcmi_result_sizes(const mcmi_result* r, int64_t* n, int64_t* nnz) {
     if (!r) return MCMI_EINVAL;
     if (n) *n = r->n;

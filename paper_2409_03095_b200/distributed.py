@@ -23,18 +23,18 @@ import numpy as np
 
 def partition_rows(row_ptr: np.ndarray, world: int) -> list[tuple[int, int]]:
     """Contiguous row blocks balanced on cost(r) = 1 + nnz(r) (a proxy for
-    the walk work of a row: steps scale with the reachable neighbourhood)."""
-    rp = np.asarray(row_ptr, np.int64)
+    the walk work of a row: steps scale with the reachable neighbourhood).
+    The library's own partition (``mcmi_partition_rows``), so one process per
+    GPU and one process over several GPUs (``McConfig.n_gpus``) cut the same
+    blocks."""
+    from . import _lib as L
+    rp = np.ascontiguousarray(row_ptr, np.int64)
     n = rp.size - 1
-    cost = np.arange(n + 1, dtype=np.float64) + rp.astype(np.float64)  # prefix of 1 + nnz(r)
-    total = cost[-1]
-    edges = [0]
-    for g in range(1, world):
-        edges.append(int(np.searchsorted(cost, total * g / world, side="left")))
-    edges.append(n)
-    for g in range(1, len(edges)):
-        edges[g] = max(edges[g], edges[g - 1])
-    return [(edges[g], edges[g + 1]) for g in range(world)]
+    edges = np.zeros(world + 1, np.int64)
+    code = L.load().mcmi_partition_rows(rp.ctypes.data, 0, n, int(world), edges.ctypes.data)
+    if code != L.MCMI_OK:
+        raise ValueError(f"mcmi_partition_rows failed with status {code}")
+    return [(int(edges[g]), int(edges[g + 1])) for g in range(world)]
 
 
 def _gather_padded(t, dist, group=None):

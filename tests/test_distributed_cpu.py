@@ -70,3 +70,40 @@ def test_partition_rows_balanced_and_contiguous():
         assert all(parts[g][1] == parts[g + 1][0] for g in range(world - 1))
         cost = [(hi - lo) + int(rp[hi] - rp[lo]) for lo, hi in parts]
         assert max(cost) - min(cost) <= 2 * (1 + int(np.diff(rp).max()))
+
+
+def _partition_numpy(rp, lo, hi, world):
+    """Restatement of the partition rule: block g starts at the first row whose
+    cost prefix (cost = 1 + nnz per row) reaches total * g / world."""
+    rp = np.asarray(rp, np.int64)
+    idx = np.arange(lo, hi + 1)
+    cost = (idx - lo).astype(np.float64) + (rp[lo:hi + 1] - rp[lo]).astype(np.float64)
+    total = cost[-1] if hi > lo else 0.0
+    edges = [lo]
+    for g in range(1, world):
+        e = lo + int(np.searchsorted(cost, total * g / world, side="left")) if hi > lo else lo
+        edges.append(max(min(e, hi), edges[-1]))
+    edges.append(hi)
+    return edges
+
+
+def test_library_partition_matches_restatement():
+    """mcmi_partition_rows (used by host builds over several GPUs and by
+    distributed.partition_rows) against the numpy restatement: sub-ranges,
+    empty rows, more parts than rows."""
+    from paper_2409_03095_b200 import _lib as L
+    lib = L.load()
+    rng = np.random.default_rng(3)
+    for trial in range(60):
+        n = int(rng.integers(0, 400))
+        deg = rng.integers(0, 40, size=n) * (rng.random(n) < 0.8)
+        rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+        lo = int(rng.integers(0, n + 1))
+        hi = int(rng.integers(lo, n + 1))
+        world = int(rng.integers(1, 12))
+        edges = np.zeros(world + 1, np.int64)
+        assert lib.mcmi_partition_rows(rp.ctypes.data, lo, hi, world, edges.ctypes.data) == L.MCMI_OK
+        assert edges.tolist() == _partition_numpy(rp, lo, hi, world), (trial, n, lo, hi, world)
+    bad = np.zeros(3, np.int64)
+    assert lib.mcmi_partition_rows(bad.ctypes.data, 0, 2, 0, bad.ctypes.data) == L.MCMI_EINVAL
+    assert lib.mcmi_partition_rows(bad.ctypes.data, 2, 1, 2, bad.ctypes.data) == L.MCMI_EINVAL
