@@ -1058,6 +1058,7 @@ void mcmi_config_default(mcmi_config* c) {
 const char* mcmi_version(void) { return "mcmi 1 sm_100a"; }
 
 int mcmi_engine_create(int device, mcmi_engine** out, char* err, size_t errlen) {
+    const mcmi::DeviceGuard device_guard;
     *out = nullptr;
     auto* e = new mcmi_engine();
     Status st = engine_init(e, device);
@@ -1071,6 +1072,7 @@ int mcmi_engine_create(int device, mcmi_engine** out, char* err, size_t errlen) 
 }
 
 void mcmi_engine_destroy(mcmi_engine* e) {
+    const mcmi::DeviceGuard device_guard;
     if (!e) return;
     engine_release(e);
     delete e;
@@ -1079,6 +1081,7 @@ void mcmi_engine_destroy(mcmi_engine* e) {
 int mcmi_engine_build(mcmi_engine* e, const mcmi_csr_view* b, const mcmi_config* cfg,
                       int64_t row_begin, int64_t row_end, void* stream, mcmi_device_csr* out,
                       mcmi_stats* stats, char* err, size_t errlen) {
+    const mcmi::DeviceGuard device_guard;
     if (!e || !b || !cfg || !out) return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
     cudaStream_t s = stream ? static_cast<cudaStream_t>(stream) : e->own;
     return report(engine_build(e, *b, *cfg, row_begin, row_end, s, out, stats), err, errlen);
@@ -1091,6 +1094,7 @@ int mcmi_build(const mcmi_csr_view* b, const mcmi_config* cfg, mcmi_result** out
 
 int mcmi_build_rows(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_begin,
                     int64_t row_end, mcmi_result** out, char* err, size_t errlen) {
+    const mcmi::DeviceGuard device_guard;
     *out = nullptr;
     if (!b || !cfg) return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
     auto* r = new mcmi_result();
@@ -1107,6 +1111,7 @@ int mcmi_build_into(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_
                     int64_t* row_ptr, int64_t* col_idx, double* values, int64_t capacity,
                     int64_t* chains_used, int64_t* entries_before, int64_t* nnz, mcmi_stats* stats,
                     char* err, size_t errlen) {
+    const mcmi::DeviceGuard device_guard;
     if (!b || !cfg || !row_ptr || !nnz || (capacity > 0 && (!col_idx || !values)))
         return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
     std::vector<int> devs;
@@ -1162,6 +1167,7 @@ int mcmi_result_sizes(const mcmi_result* r, int64_t* n, int64_t* nnz) {
 int mcmi_result_copy(const mcmi_result* r, int64_t* row_ptr, int64_t* col_idx, double* values,
                      int64_t* chains_used, int64_t* entries_before, int64_t* n_chains,
                      int64_t* max_len) {
+    const mcmi::DeviceGuard device_guard;
     if (!r) return MCMI_EINVAL;
     const int code = copy_parts(r, row_ptr, col_idx, values, chains_used, entries_before);
     if (n_chains) *n_chains = r->n_chains;
@@ -1176,6 +1182,7 @@ int mcmi_result_stats(const mcmi_result* r, mcmi_stats* stats) {
 }
 
 void mcmi_result_free(mcmi_result* r) {
+    const mcmi::DeviceGuard device_guard;
     if (!r) return;
     free_parts(r);
     delete r;

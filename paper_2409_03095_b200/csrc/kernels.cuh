@@ -11,6 +11,24 @@
 namespace mcmi {
 
 // Device-side scalar reductions and error slots of one build (zeroed per build).
+// Restores the calling thread's current CUDA device when a C-ABI entry point
+// returns: the library switches devices internally (engines, shards), callers
+// (PyTorch, a reference-side host program) must not see it.
+struct DeviceGuard {
+    int prev = -1;
+    DeviceGuard() {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            prev = -1;
+            cudaGetLastError();
+        }
+    }
+    ~DeviceGuard() {
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    DeviceGuard(const DeviceGuard&) = delete;
+    DeviceGuard& operator=(const DeviceGuard&) = delete;
+};
+
 struct Reductions {
     unsigned long long offmin_bits;  // min |b_ij| over off-diagonals (csr.cpp:88-105)
     unsigned long long offmax_bits;  // max |b_ij| over off-diagonals

@@ -301,6 +301,7 @@ extern "C" {
 
 int mcmi_recover_inverse_device(double* m_dev, int64_t n, const double* s_diag, int64_t s_len, double tol,
                                 int device, void* stream, char* err, size_t errlen) {
+    const mcmi::DeviceGuard device_guard;
     std::string msg;
     int code = check_args(n, s_diag, s_len, tol, msg);
     if (code) return finish(code, msg, err, errlen);
@@ -313,6 +314,7 @@ int mcmi_recover_inverse_device(double* m_dev, int64_t n, const double* s_diag, 
 
 int mcmi_recover_inverse(double* m, int64_t n, const double* s_diag, int64_t s_len, double tol, int device,
                          char* err, size_t errlen) {
+    const mcmi::DeviceGuard device_guard;
     std::string msg;
     int code = check_args(n, s_diag, s_len, tol, msg);
     if (code) return finish(code, msg, err, errlen);

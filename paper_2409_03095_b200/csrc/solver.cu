@@ -614,6 +614,7 @@ void mcmi_solver_config_default(mcmi_solver_config* c) {
 int mcmi_solve_device(const mcmi_csr_view* b, const mcmi_csr_view* m, const double* rhs, double* x,
                       const mcmi_solver_config* cfg, int device, void* stream, mcmi_solve_report* rep,
                       char* err, size_t errlen) {
+    const mcmi::DeviceGuard device_guard;
     std::string msg;
     int code = MCMI_OK;
     if (!b || !x || !cfg || !rep) {
