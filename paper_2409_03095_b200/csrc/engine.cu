@@ -494,15 +494,21 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         wa.gscratch = nullptr;
         int64_t max_warps = 0;
         if (t.global) {
-            size_t free_b = 0, total_b = 0;
-            MCMI_TRY(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
             const size_t per_warp = walk_global_bytes_per_warp(t.cap, t.lanes, t.log_stride);
-            const size_t budget = std::min<size_t>(size_t{16} << 30, free_b / 2);
-            max_warps = std::min<int64_t>(static_cast<int64_t>(budget / per_warp),
-                                          static_cast<int64_t>(e->num_sms) * 32);
-            if (max_warps < 1) return fail(MCMI_ENOMEM, "accumulator row too large for device memory");
-            max_warps = std::max<int64_t>(8, max_warps / 8 * 8);
-            MCMI_TRY(e->gscratch.ensure(static_cast<size_t>(max_warps) * per_warp), "alloc accumulator scratch");
+            const int64_t full = static_cast<int64_t>(e->num_sms) * 32;  // 32 warps/SM
+            if (e->gscratch.cap >= static_cast<size_t>(full) * per_warp) {
+                // the scratch already holds every resident warp's table: no
+                // cudaMemGetInfo (it can stall for tens of ms behind the driver)
+                max_warps = full;
+            } else {
+                size_t free_b = 0, total_b = 0;
+                MCMI_TRY(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+                const size_t budget = std::min<size_t>(size_t{16} << 30, (free_b + e->gscratch.cap) / 2);
+                max_warps = std::min<int64_t>(static_cast<int64_t>(budget / per_warp), full);
+                if (max_warps < 1) return fail(MCMI_ENOMEM, "accumulator row too large for device memory");
+                max_warps = std::max<int64_t>(8, max_warps / 8 * 8);
+                MCMI_TRY(e->gscratch.ensure(static_cast<size_t>(max_warps) * per_warp), "alloc accumulator scratch");
+            }
             wa.gscratch = e->gscratch.as<unsigned char>();
         }
         wa.stage_col = e->stage_col.as<int>();
