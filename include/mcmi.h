@@ -84,6 +84,10 @@ typedef struct mcmi_config {
 /* flags */
 #define MCMI_FLAG_DEG_STATS 1 /* also count sum of deg(s) over walk steps (mcmi_stats.walk_deg_sum);
                                  costs ~4% walk throughput (registers), so it is opt-in */
+#define MCMI_FLAG_UNSCALED 2  /* rows of (I - A)^-1 as mcspai::estimate_row returns them
+                                 (mc_engine.hpp:57-65): no scale_columns, no zero prune.  With
+                                 retain_k = 0 and rows (r, r+1) this is estimate_row(split, r,
+                                 budget, delta, RngStream(master_seed, r)). */
 
 /* Fills cfg with the reference defaults (McConfig{}). */
 void mcmi_config_default(mcmi_config* cfg);
@@ -142,6 +146,43 @@ int mcmi_build_into(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_
                     int64_t* row_ptr, int64_t* col_idx, double* values, int64_t capacity,
                     int64_t* chains_used, int64_t* entries_before, int64_t* nnz, mcmi_stats* stats,
                     char* err, size_t errlen);
+/* ------------------------------------------- fine-grained pipeline stages */
+/* The reference's public building blocks, on the same device
+ * code as the build.  retain_top_k / scale_columns are fused into the walk's
+ * per-row finalize (MCMI_FLAG_UNSCALED returns the rows before them). */
+
+/* mcspai::derive_chain_budget (mc_engine.hpp:55, mc_engine.cpp:12-33), host
+ * arithmetic (glibc log / ceil) as in the build.  MCMI_EINVAL: "||A|| must lie
+ * in [0,1)". */
+int mcmi_derive_chain_budget(const mcmi_config* cfg, double a_norm, int64_t* n_chains, int64_t* max_len, char* err,
+                             size_t errlen);
+
+/* mcspai::augment_and_split (split.hpp:34-35, split.cpp:46-100) with
+ * transition_probabilities (split.cpp:102-119), computed on `device`; the
+ * result is copied to host memory.  Errors: MCMI_EINVAL "alpha must be
+ * positive"; MCMI_ESPLIT degenerate diagonal / dominance failure (the
+ * reference's messages); MCMI_ERANGE for a column outside [0, n) (the
+ * reference does not check). */
+typedef struct mcmi_split_system mcmi_split_system;
+int mcmi_augment_and_split(const mcmi_csr_view* b, double alpha, int32_t mode, int device, mcmi_split_system** out,
+                           char* err, size_t errlen);
+/* n, entries of b_hat and of A (P has A's pattern), ||A||inf */
+int mcmi_split_sizes(const mcmi_split_system* s, int64_t* n, int64_t* nnz_b_hat, int64_t* nnz_a, double* a_norm);
+/* Any pointer may be NULL.  b_hat: row_ptr[n+1], col_idx / values[nnz_b_hat];
+ * b1_diag[n]; A: row_ptr[n+1], col_idx / values[nnz_a]; p_values[nnz_a];
+ * s_diag[n] (SplitSystem, split.hpp:21-28). */
+int mcmi_split_copy(const mcmi_split_system* s, int64_t* b_hat_row_ptr, int64_t* b_hat_col_idx, double* b_hat_values,
+                    double* b1_diag, int64_t* a_row_ptr, int64_t* a_col_idx, double* a_values, double* p_values,
+                    double* s_diag);
+void mcmi_split_free(mcmi_split_system* s);
+
+/* mcspai::transition_probabilities (split.hpp:39) of any CSR A on `device`:
+ * p_ij = |a_ij| / sequential row sum; rows summing to 0 become empty.
+ * p_row_ptr[n+1]; p_col_idx / p_values hold nnz(A) entries; *p_nnz = entries
+ * written. */
+int mcmi_transition_probabilities(const mcmi_csr_view* a, int device, int64_t* p_row_ptr, int64_t* p_col_idx,
+                                  double* p_values, int64_t* p_nnz, char* err, size_t errlen);
+
 /* Row blocks of a sharded build: edges[0..parts] with block g =
  * rows [edges[g], edges[g+1]) of [row_begin, row_end), balanced on cost(r) =
  * 1 + nnz(r); edges[g] (0 < g < parts) is the first row whose cost prefix

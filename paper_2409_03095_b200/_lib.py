@@ -23,7 +23,8 @@ EXPORTS = [
     "mcmi_engine_build", "mcmi_copy", "mcmi_version", "mcmi_solver_config_default", "mcmi_solve_device",
     "mcmi_host_register", "mcmi_host_unregister", "mcmi_from_triplets", "mcmi_mm_parse", "mcmi_mm_read_file",
     "mcmi_host_csr_get", "mcmi_host_csr_free", "mcmi_mm_format", "mcmi_mm_write_file", "mcmi_recover_inverse",
-    "mcmi_recover_inverse_device", "mcmi_scatter_shard",
+    "mcmi_recover_inverse_device", "mcmi_scatter_shard", "mcmi_derive_chain_budget", "mcmi_augment_and_split",
+    "mcmi_split_sizes", "mcmi_split_copy", "mcmi_split_free", "mcmi_transition_probabilities",
 ]
 
 
@@ -49,6 +50,7 @@ class mcmi_config(C.Structure):
 
 
 MCMI_FLAG_DEG_STATS = 1
+MCMI_FLAG_UNSCALED = 2
 
 
 class mcmi_csr_view(C.Structure):
@@ -126,6 +128,15 @@ def load(path: str | None = None):
                                   C.POINTER(C.c_int64), C.POINTER(mcmi_stats), C.c_char_p, C.c_size_t]
     L.mcmi_partition_rows.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int, C.c_void_p]
     L.mcmi_result_sizes.argtypes = [C.c_void_p, _i64p, _i64p]
+    L.mcmi_derive_chain_budget.argtypes = [C.c_void_p, C.c_double, _i64p, _i64p, C.c_char_p, C.c_size_t]
+    L.mcmi_augment_and_split.argtypes = [C.c_void_p, C.c_double, C.c_int32, C.c_int, C.POINTER(C.c_void_p),
+                                         C.c_char_p, C.c_size_t]
+    L.mcmi_split_sizes.argtypes = [C.c_void_p, _i64p, _i64p, _i64p, _f64p]
+    L.mcmi_split_copy.argtypes = [C.c_void_p] + [C.c_void_p] * 9
+    L.mcmi_split_free.argtypes = [C.c_void_p]
+    L.mcmi_split_free.restype = None
+    L.mcmi_transition_probabilities.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, _i64p,
+                                                C.c_char_p, C.c_size_t]
     L.mcmi_result_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    _i64p, _i64p]
     L.mcmi_result_stats.argtypes = [C.c_void_p, C.POINTER(mcmi_stats)]

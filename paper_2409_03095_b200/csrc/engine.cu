@@ -491,6 +491,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         wa.log_magic = static_cast<unsigned>((0x100000000ull + t.log_stride - 1) / t.log_stride);
         wa.ell0 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(L, 2)));
         wa.deg_stats = (cfg.flags & MCMI_FLAG_DEG_STATS) ? 1 : 0;
+        wa.unscaled = (cfg.flags & MCMI_FLAG_UNSCALED) ? 1 : 0;
         wa.gscratch = nullptr;
         int64_t max_warps = 0;
         if (t.global) {
@@ -1049,6 +1050,194 @@ void free_parts(mcmi_result* r) {
 
 }  // namespace
 
+// The SplitSystem of mcmi_augment_and_split, copied to host memory.
+struct mcmi_split_system {
+    int64_t n = 0, nnz_bh = 0, nnz_a = 0;
+    double a_norm = 0.0;
+    std::vector<int64_t> bh_rp, bh_ci, a_rp, a_ci;
+    std::vector<double> bh_v, b1, a_v, p_v, s_diag;
+};
+
+namespace {
+
+// Stream-ordered device temporaries of one fine-grained call (freed on scope exit).
+struct DevTemps {
+    cudaStream_t s;
+    std::vector<void*> ptrs;
+    cudaError_t err = cudaSuccess;
+    explicit DevTemps(cudaStream_t st) : s(st) {}
+    template <class T>
+    T* get(int64_t count) {
+        void* p = nullptr;
+        if (err == cudaSuccess) err = cudaMallocAsync(&p, static_cast<size_t>(std::max<int64_t>(count, 1)) * sizeof(T), s);
+        if (p) ptrs.push_back(p);
+        return static_cast<T*>(p);
+    }
+    ~DevTemps() {
+        for (void* p : ptrs) cudaFreeAsync(p, s);
+        cudaStreamSynchronize(s);
+    }
+};
+
+Status check_host_view(const mcmi_csr_view* b) {
+    if (!b) return fail(MCMI_EINVAL, "null argument");
+    if (b->n < 0) return fail(MCMI_EINVAL, "negative dimension");
+    if (b->n > 0 && !b->row_ptr) return fail(MCMI_EINVAL, "null row_ptr");
+    const int64_t nnz = b->n > 0 ? b->row_ptr[b->n] : 0;
+    if (nnz < 0) return fail(MCMI_EINVAL, "row_ptr[n] is negative");
+    if (nnz > 0 && (!b->col_idx || !b->values)) return fail(MCMI_EINVAL, "null col_idx / values");
+    return ok();
+}
+
+// Stages a host CSR on the engine's stream and validates its row pointer.
+Status stage_csr(mcmi_engine* e, const mcmi_csr_view& b, DevTemps& t, mcmi_csr_view* dv) {
+    const int64_t n = b.n, nnz = n > 0 ? b.row_ptr[n] : 0;
+    cudaStream_t s = e->own;
+    auto* rp = t.get<int64_t>(n + 1);
+    auto* ci = t.get<int64_t>(nnz);
+    auto* v = t.get<double>(nnz);
+    MCMI_TRY(t.err, "alloc staging");
+    MCMI_TRY(cudaMemcpyAsync(rp, b.row_ptr, (n + 1) * sizeof(int64_t), cudaMemcpyDefault, s), "H2D");
+    if (nnz) {
+        MCMI_TRY(cudaMemcpyAsync(ci, b.col_idx, nnz * sizeof(int64_t), cudaMemcpyDefault, s), "H2D");
+        MCMI_TRY(cudaMemcpyAsync(v, b.values, nnz * sizeof(double), cudaMemcpyDefault, s), "H2D");
+    }
+    MCMI_TRY(e->red.ensure(sizeof(Reductions)), "alloc reductions");
+    Reductions init{};
+    init.offmin_bits = 0x7ff0000000000000ull;
+    init.degenerate_row = LLONG_MAX;
+    init.bad_col_row = LLONG_MAX;
+    init.bad_rowptr_row = LLONG_MAX;
+    *e->h_red = init;
+    MCMI_TRY(cudaMemcpyAsync(e->red.p, e->h_red, sizeof(Reductions), cudaMemcpyHostToDevice, s), "init reductions");
+    MCMI_TRY(launch_validate_row_ptr(rp, n, nnz, e->red.as<Reductions>(), s), "validate row_ptr");
+    MCMI_TRY(cudaMemcpyAsync(e->h_red, e->red.p, sizeof(Reductions), cudaMemcpyDeviceToHost, s), "read validation");
+    MCMI_TRY(cudaStreamSynchronize(s), "validate row_ptr");
+    if (e->h_red->bad_rowptr_row != LLONG_MAX)
+        return fail(MCMI_EINVAL,
+                    "row_ptr is not a valid CSR row pointer at row " + std::to_string(e->h_red->bad_rowptr_row));
+    *dv = mcmi_csr_view{n, rp, ci, v};
+    return ok();
+}
+
+template <class T>
+Status d2h_vec(std::vector<T>& dst, const T* src, int64_t count, cudaStream_t s) {
+    dst.resize(static_cast<size_t>(std::max<int64_t>(count, 0)));
+    if (count > 0) MCMI_TRY(cudaMemcpyAsync(dst.data(), src, count * sizeof(T), cudaMemcpyDeviceToHost, s), "D2H");
+    return ok();
+}
+
+Status augment_and_split_dev(mcmi_engine* e, const mcmi_csr_view& b, double alpha, int mode,
+                             mcmi_split_system* out) {
+    if (!(alpha > 0.0)) return fail(MCMI_EINVAL, "alpha must be positive");  // split.cpp:48
+    MCMI_TRY(cudaSetDevice(e->device), "cudaSetDevice");
+    cudaStream_t s = e->own;
+    DevTemps t(s);
+    mcmi_csr_view dv{};
+    if (Status st = stage_csr(e, b, t, &dv); st.code) return st;
+    const int64_t n = b.n;
+    SplitExportArgs a{};
+    a.n = n;
+    a.row_ptr = dv.row_ptr;
+    a.col_idx = dv.col_idx;
+    a.values = dv.values;
+    a.alpha = alpha;
+    a.mode = mode;
+    a.red = e->red.as<Reductions>();
+    a.diag_val = t.get<double>(n);
+    a.has_diag = t.get<unsigned char>(n);
+    a.bh_cnt = t.get<int>(n);
+    a.a_cnt = t.get<int>(n);
+    a.b1_diag = t.get<double>(n);
+    a.s_diag = t.get<double>(n);
+    int64_t* bh_rp = t.get<int64_t>(n + 1);
+    int64_t* a_rp = t.get<int64_t>(n + 1);
+    a.bh_row_ptr = bh_rp;
+    a.a_row_ptr = a_rp;
+    MCMI_TRY(t.err, "alloc split");
+    MCMI_TRY(e->scan_tmp.ensure(scan_scratch_bytes(std::max<int64_t>(n, 1)) + 64), "alloc scan");
+    MCMI_TRY(launch_split_export(a, 0, s), "split kernels");
+    MCMI_TRY(cudaMemcpyAsync(e->h_red, e->red.p, sizeof(Reductions), cudaMemcpyDeviceToHost, s), "read split");
+    MCMI_TRY(cudaStreamSynchronize(s), "split kernels");
+    const Reductions red = *e->h_red;
+    if (red.bad_col_row != LLONG_MAX)
+        return fail(MCMI_ERANGE, "column index out of range in row " + std::to_string(red.bad_col_row));
+    if (red.degenerate_row != LLONG_MAX)  // split.cpp:67-69
+        return fail(MCMI_ESPLIT, "degenerate diagonal after augmentation at row " + std::to_string(red.degenerate_row));
+    double a_norm;
+    std::memcpy(&a_norm, &red.anorm_bits, sizeof(double));
+    if (!(a_norm < 1.0))  // split.cpp:94-96
+        return fail(MCMI_ESPLIT, "diagonal dominance failure: ||A||inf = " + std::to_string(a_norm));
+    MCMI_TRY(scan_rows_exclusive(a.bh_cnt, bh_rp, n, e->scan_tmp.p, s), "scan");
+    MCMI_TRY(scan_rows_exclusive(a.a_cnt, a_rp, n, e->scan_tmp.p, s), "scan");
+    int64_t tot[2] = {0, 0};
+    MCMI_TRY(cudaMemcpyAsync(&tot[0], bh_rp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+    MCMI_TRY(cudaMemcpyAsync(&tot[1], a_rp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+    MCMI_TRY(cudaStreamSynchronize(s), "scan");
+    a.bh_col = t.get<int64_t>(tot[0]);
+    a.bh_val = t.get<double>(tot[0]);
+    a.a_col = t.get<int64_t>(tot[1]);
+    a.a_val = t.get<double>(tot[1]);
+    a.p_val = t.get<double>(tot[1]);
+    MCMI_TRY(t.err, "alloc split");
+    MCMI_TRY(launch_split_export(a, 1, s), "split fill");
+    out->n = n;
+    out->nnz_bh = tot[0];
+    out->nnz_a = tot[1];
+    out->a_norm = a_norm;
+    Status st;
+    for (Status x : {d2h_vec(out->bh_rp, static_cast<const int64_t*>(bh_rp), n + 1, s),
+                     d2h_vec(out->bh_ci, static_cast<const int64_t*>(a.bh_col), tot[0], s),
+                     d2h_vec(out->bh_v, static_cast<const double*>(a.bh_val), tot[0], s),
+                     d2h_vec(out->b1, static_cast<const double*>(a.b1_diag), n, s),
+                     d2h_vec(out->s_diag, static_cast<const double*>(a.s_diag), n, s),
+                     d2h_vec(out->a_rp, static_cast<const int64_t*>(a_rp), n + 1, s),
+                     d2h_vec(out->a_ci, static_cast<const int64_t*>(a.a_col), tot[1], s),
+                     d2h_vec(out->a_v, static_cast<const double*>(a.a_val), tot[1], s),
+                     d2h_vec(out->p_v, static_cast<const double*>(a.p_val), tot[1], s)})
+        if (x.code && !st.code) st = x;
+    if (st.code) return st;
+    MCMI_TRY(cudaStreamSynchronize(s), "split D2H");
+    if (n == 0) out->bh_rp.assign(1, 0), out->a_rp.assign(1, 0);
+    return ok();
+}
+
+Status transition_probabilities_dev(mcmi_engine* e, const mcmi_csr_view& a, int64_t* p_rp, int64_t* p_ci,
+                                    double* p_v, int64_t* p_nnz) {
+    MCMI_TRY(cudaSetDevice(e->device), "cudaSetDevice");
+    cudaStream_t s = e->own;
+    DevTemps t(s);
+    mcmi_csr_view dv{};
+    if (Status st = stage_csr(e, a, t, &dv); st.code) return st;
+    const int64_t n = a.n;
+    int* cnt = t.get<int>(n);
+    int64_t* orp = t.get<int64_t>(n + 1);
+    MCMI_TRY(t.err, "alloc");
+    MCMI_TRY(e->scan_tmp.ensure(scan_scratch_bytes(std::max<int64_t>(n, 1)) + 64), "alloc scan");
+    MCMI_TRY(launch_transition_probabilities(dv.row_ptr, dv.col_idx, dv.values, n, cnt, nullptr, nullptr, nullptr, 0, s),
+             "transition counts");
+    MCMI_TRY(scan_rows_exclusive(cnt, orp, n, e->scan_tmp.p, s), "scan");
+    int64_t tot = 0;
+    MCMI_TRY(cudaMemcpyAsync(&tot, orp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+    MCMI_TRY(cudaStreamSynchronize(s), "scan");
+    int64_t* oci = t.get<int64_t>(tot);
+    double* ov = t.get<double>(tot);
+    MCMI_TRY(t.err, "alloc");
+    MCMI_TRY(launch_transition_probabilities(dv.row_ptr, dv.col_idx, dv.values, n, nullptr, orp, oci, ov, 1, s),
+             "transition fill");
+    MCMI_TRY(cudaMemcpyAsync(p_rp, orp, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+    if (tot) {
+        MCMI_TRY(cudaMemcpyAsync(p_ci, oci, tot * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+        MCMI_TRY(cudaMemcpyAsync(p_v, ov, tot * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    }
+    MCMI_TRY(cudaStreamSynchronize(s), "D2H");
+    if (n == 0) p_rp[0] = 0;
+    *p_nnz = tot;
+    return ok();
+}
+
+}  // namespace
+
 extern "C" {
 
 void mcmi_config_default(mcmi_config* c) {
@@ -1152,6 +1341,77 @@ int mcmi_build_into(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_
     st = build_from_host(e, *b, c, row_begin, row_end, &dc, &ls, &sink);
     *nnz = ls.nnz;
     if (stats) *stats = ls;
+    release_engine(e);
+    return report(st, err, errlen);
+}
+
+int mcmi_derive_chain_budget(const mcmi_config* cfg, double a_norm, int64_t* n_chains, int64_t* max_len, char* err,
+                             size_t errlen) {
+    if (!cfg || !n_chains || !max_len) return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    return report(chain_budget(*cfg, a_norm, n_chains, max_len), err, errlen);
+}
+
+int mcmi_augment_and_split(const mcmi_csr_view* b, double alpha, int32_t mode, int device, mcmi_split_system** out,
+                           char* err, size_t errlen) {
+    const mcmi::DeviceGuard device_guard;
+    if (!out) return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    *out = nullptr;
+    if (Status st = check_host_view(b); st.code) return report(st, err, errlen);
+    Status st;
+    mcmi_engine* e = acquire_engine(device, &st);
+    if (!e) return report(st, err, errlen);
+    auto* r = new mcmi_split_system();
+    st = augment_and_split_dev(e, *b, alpha, mode, r);
+    release_engine(e);
+    if (st.code) {
+        delete r;
+        return report(st, err, errlen);
+    }
+    *out = r;
+    return MCMI_OK;
+}
+
+int mcmi_split_sizes(const mcmi_split_system* s, int64_t* n, int64_t* nnz_b_hat, int64_t* nnz_a, double* a_norm) {
+    if (!s) return MCMI_EINVAL;
+    if (n) *n = s->n;
+    if (nnz_b_hat) *nnz_b_hat = s->nnz_bh;
+    if (nnz_a) *nnz_a = s->nnz_a;
+    if (a_norm) *a_norm = s->a_norm;
+    return MCMI_OK;
+}
+
+int mcmi_split_copy(const mcmi_split_system* s, int64_t* b_hat_row_ptr, int64_t* b_hat_col_idx, double* b_hat_values,
+                    double* b1_diag, int64_t* a_row_ptr, int64_t* a_col_idx, double* a_values, double* p_values,
+                    double* s_diag) {
+    if (!s) return MCMI_EINVAL;
+    auto cp = [](void* dst, const void* src, size_t bytes) {
+        if (dst && bytes) std::memcpy(dst, src, bytes);
+    };
+    cp(b_hat_row_ptr, s->bh_rp.data(), s->bh_rp.size() * sizeof(int64_t));
+    cp(b_hat_col_idx, s->bh_ci.data(), s->bh_ci.size() * sizeof(int64_t));
+    cp(b_hat_values, s->bh_v.data(), s->bh_v.size() * sizeof(double));
+    cp(b1_diag, s->b1.data(), s->b1.size() * sizeof(double));
+    cp(a_row_ptr, s->a_rp.data(), s->a_rp.size() * sizeof(int64_t));
+    cp(a_col_idx, s->a_ci.data(), s->a_ci.size() * sizeof(int64_t));
+    cp(a_values, s->a_v.data(), s->a_v.size() * sizeof(double));
+    cp(p_values, s->p_v.data(), s->p_v.size() * sizeof(double));
+    cp(s_diag, s->s_diag.data(), s->s_diag.size() * sizeof(double));
+    return MCMI_OK;
+}
+
+void mcmi_split_free(mcmi_split_system* s) { delete s; }
+
+int mcmi_transition_probabilities(const mcmi_csr_view* a, int device, int64_t* p_row_ptr, int64_t* p_col_idx,
+                                  double* p_values, int64_t* p_nnz, char* err, size_t errlen) {
+    const mcmi::DeviceGuard device_guard;
+    if (!p_row_ptr || !p_nnz) return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    if (Status st = check_host_view(a); st.code) return report(st, err, errlen);
+    if (a->n > 0 && a->row_ptr[a->n] > 0 && (!p_col_idx || !p_values))
+        return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    Status st;
+    mcmi_engine* e = acquire_engine(device, &st);
+    if (!e) return report(st, err, errlen);
+    st = transition_probabilities_dev(e, *a, p_row_ptr, p_col_idx, p_values, p_nnz);
     release_engine(e);
     return report(st, err, errlen);
 }

@@ -10,7 +10,6 @@
 
 namespace mcmi {
 
-// Device-side scalar reductions and error slots of one build (zeroed per build).
 // Restores the calling thread's current CUDA device when a C-ABI entry point
 // returns: the library switches devices internally (engines, shards), callers
 // (PyTorch, a reference-side host program) must not see it.
@@ -29,6 +28,7 @@ struct DeviceGuard {
     DeviceGuard& operator=(const DeviceGuard&) = delete;
 };
 
+// Device-side scalar reductions and error slots of one build (zeroed per build).
 struct Reductions {
     unsigned long long offmin_bits;  // min |b_ij| over off-diagonals (csr.cpp:88-105)
     unsigned long long offmax_bits;  // max |b_ij| over off-diagonals
@@ -82,6 +82,30 @@ struct TableBuildArgs {
     double* b1_diag;
 };
 
+// The SplitSystem as matrices (mcmi_augment_and_split).
+struct SplitExportArgs {
+    int64_t n;
+    const int64_t* row_ptr;
+    const int64_t* col_idx;
+    const double* values;
+    double alpha;
+    int mode;
+    Reductions* red;
+    double* diag_val;          // [n]
+    unsigned char* has_diag;   // [n]
+    int* bh_cnt;               // [n] b_hat row lengths
+    int* a_cnt;                // [n] A row lengths
+    double* b1_diag;           // [n]
+    double* s_diag;            // [n]
+    const int64_t* bh_row_ptr; // [n+1] (pass 1)
+    const int64_t* a_row_ptr;  // [n+1] (pass 1)
+    int64_t* bh_col;
+    double* bh_val;
+    int64_t* a_col;
+    double* a_val;
+    double* p_val;
+};
+
 // Walk + accumulate + per-row finalize (subsystems 2 and 3).
 struct WalkArgs {
     Tables t;
@@ -105,6 +129,7 @@ struct WalkArgs {
     int log_shift;          // launch_walk: log2(log_stride) if a power of two, else -1
     long long warp_bytes;   // launch_walk: shared/global bytes per warp
     int deg_stats;          // count sum deg(s) (MCMI_FLAG_DEG_STATS)
+    int unscaled;           // MCMI_FLAG_UNSCALED: rows of (I - A)^-1 (estimate_row), no scale / prune
     unsigned char* gscratch;  // global-tier per-warp accumulator + log (nullptr for smem tiers)
     // outputs, indexed by local row (row - row_begin)
     int* stage_col;
@@ -124,6 +149,12 @@ cudaError_t launch_validate_row_ptr(const int64_t* row_ptr, int64_t n, int64_t n
 cudaError_t launch_table_build(const TableBuildArgs& a, int64_t nnz, bool drop_active,
                                cudaStream_t s);
 cudaError_t launch_table_fill(const TableBuildArgs& a, cudaStream_t s);
+// pass 0: norms, diagonal, row counts, ||A||; pass 1: fill b_hat / A / P.
+cudaError_t launch_split_export(const SplitExportArgs& a, int pass, cudaStream_t s);
+// pass 0: row counts into cnt; pass 1: fill with out_rp (exclusive scan of cnt).
+cudaError_t launch_transition_probabilities(const int64_t* rp, const int64_t* ci, const double* v, int64_t n,
+                                            int* cnt, const int64_t* out_rp, int64_t* out_ci, double* out_v,
+                                            int pass, cudaStream_t s);
 cudaError_t launch_count_quantile(const TableBuildArgs& a, int64_t nnz, int64_t n_drop,
                                   void* scratch, size_t scratch_bytes, cudaStream_t s);
 size_t count_quantile_scratch_bytes(int64_t nnz);

@@ -399,6 +399,140 @@ __global__ void k_cq_keep(TableBuildArgs a, const CqState* st, const unsigned* t
         }
 }
 
+
+// ---- the SplitSystem as matrices (mcmi_augment_and_split, §8b fine-grained
+// API): the same per-row arithmetic as the table build, written out as the
+// reference's b_hat / A / P CSRs (split.cpp:46-119), no drop.
+
+// Pass 1: ||B||inf (inf_norm over all stored entries, csr.cpp:77-86), the
+// first diagonal entry (with_explicit_diagonal: 0 if absent), b_hat's row
+// lengths (one inserted diagonal where absent), column range.
+__global__ void k_sx_norm(SplitExportArgs a) {
+    double best = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0, d = 0.0;
+        bool found = false;
+        for (int64_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
+            const int64_t c = a.col_idx[k];
+            const double v = a.values[k];
+            if (c < 0 || c >= a.n) atomicMin(&a.red->bad_col_row, static_cast<long long>(i));
+            s += fabs(v);
+            if (c == i && !found) {
+                d = v;
+                found = true;
+            }
+        }
+        a.diag_val[i] = d;
+        a.has_diag[i] = found ? 1 : 0;
+        a.bh_cnt[i] = static_cast<int>(a.row_ptr[i + 1] - a.row_ptr[i]) + (found ? 0 : 1);
+        best = fmax(best, s);
+    }
+    best = block_max(best);
+    if (threadIdx.x == 0) atomic_max_nonneg(&a.red->bnorm_bits, best);
+}
+
+// Pass 2: b1 = d + shift, s = b1 - d (split.cpp:58-66), A's row lengths and
+// ||A||inf (split.cpp:76-92).
+__global__ void k_sx_split(SplitExportArgs a) {
+    const double b_norm = __longlong_as_double(static_cast<long long>(a.red->bnorm_bits));
+    double best = 0.0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double d = a.diag_val[i];
+        double shift = a.alpha * b_norm;
+        if (a.mode == 1 && d < 0.0) shift = -shift;
+        const double b1 = d + shift;
+        a.b1_diag[i] = b1;
+        a.s_diag[i] = b1 - d;
+        if (b1 == 0.0) atomicMin(&a.red->degenerate_row, static_cast<long long>(i));
+        double row_sum = 0.0;
+        int cnt = 0;
+        for (int64_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
+            if (a.col_idx[k] == i) continue;
+            const double av = -a.values[k] / b1;
+            if (av == 0.0) continue;
+            ++cnt;
+            row_sum += fabs(av);
+        }
+        a.a_cnt[i] = cnt;
+        best = fmax(best, row_sum);
+    }
+    best = block_max(best);
+    if (threadIdx.x == 0) atomic_max_nonneg(&a.red->anorm_bits, best);
+}
+
+// Pass 3: b_hat (the first diagonal entry augmented, a missing one inserted
+// before the first larger column), A and P = transition_probabilities(A)
+// (split.cpp:102-119: |a| / sequential row sum; A has no zeros, so P has A's
+// pattern).
+__global__ void k_sx_fill(SplitExportArgs a) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double b1 = a.b1_diag[i];
+        const int64_t k0 = a.row_ptr[i], k1 = a.row_ptr[i + 1];
+        int64_t o = a.bh_row_ptr[i];
+        bool placed = a.has_diag[i] != 0;  // with_explicit_diagonal (split.cpp:22-37)
+        bool first = true;
+        for (int64_t k = k0; k < k1; ++k) {
+            const int64_t c = a.col_idx[k];
+            if (!placed && c > i) {
+                a.bh_col[o] = i;
+                a.bh_val[o++] = b1;
+                placed = true;
+            }
+            double v = a.values[k];
+            if (c == i && first) {
+                v = b1;
+                first = false;
+            }
+            a.bh_col[o] = c;
+            a.bh_val[o++] = v;
+        }
+        if (!placed) {
+            a.bh_col[o] = i;
+            a.bh_val[o] = b1;
+        }
+        double row_sum = 0.0;
+        int64_t q = a.a_row_ptr[i];
+        for (int64_t k = k0; k < k1; ++k) {
+            const int64_t c = a.col_idx[k];
+            if (c == i) continue;
+            const double av = -a.values[k] / b1;
+            if (av == 0.0) continue;
+            a.a_col[q] = c;
+            a.a_val[q++] = av;
+            row_sum += fabs(av);
+        }
+        for (int64_t j = a.a_row_ptr[i]; j < q; ++j) a.p_val[j] = fabs(a.a_val[j]) / row_sum;
+    }
+}
+
+// transition_probabilities of an arbitrary A (split.cpp:102-119): rows with
+// a zero absolute sum become empty (absorbing), the others keep A's pattern.
+__global__ void k_tp_count(const int64_t* __restrict__ rp, const double* __restrict__ v, int64_t n,
+                           int* __restrict__ cnt) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int64_t k = rp[i]; k < rp[i + 1]; ++k) s += fabs(v[k]);
+        cnt[i] = s > 0.0 ? static_cast<int>(rp[i + 1] - rp[i]) : 0;
+    }
+}
+
+__global__ void k_tp_fill(const int64_t* __restrict__ rp, const int64_t* __restrict__ ci,
+                          const double* __restrict__ v, int64_t n, const int64_t* __restrict__ out_rp,
+                          int64_t* __restrict__ out_ci, double* __restrict__ out_v) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        if (out_rp[i + 1] == out_rp[i]) continue;
+        double s = 0.0;
+        for (int64_t k = rp[i]; k < rp[i + 1]; ++k) s += fabs(v[k]);
+        int64_t o = out_rp[i];
+        for (int64_t k = rp[i]; k < rp[i + 1]; ++k) {
+            out_ci[o] = ci[k];
+            out_v[o++] = fabs(v[k]) / s;
+        }
+    }
+}
 }  // namespace
 
 size_t count_quantile_scratch_bytes(int64_t nnz) {
@@ -453,6 +587,27 @@ cudaError_t launch_table_build(const TableBuildArgs& a, int64_t /*nnz*/, bool dr
 
 cudaError_t launch_table_fill(const TableBuildArgs& a, cudaStream_t s) {
     k_rows_fill<<<grid_for(a.n), TB, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_split_export(const SplitExportArgs& a, int pass, cudaStream_t s) {
+    const int g = grid_for(a.n);
+    if (a.n <= 0) return cudaSuccess;
+    if (pass == 0) {
+        k_sx_norm<<<g, TB, 0, s>>>(a);
+        k_sx_split<<<g, TB, 0, s>>>(a);
+    } else {
+        k_sx_fill<<<g, TB, 0, s>>>(a);
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_transition_probabilities(const int64_t* rp, const int64_t* ci, const double* v, int64_t n,
+                                            int* cnt, const int64_t* out_rp, int64_t* out_ci, double* out_v,
+                                            int pass, cudaStream_t s) {
+    if (n <= 0) return cudaSuccess;
+    if (pass == 0) k_tp_count<<<grid_for(n), TB, 0, s>>>(rp, v, n, cnt);
+    else k_tp_fill<<<grid_for(n), TB, 0, s>>>(rp, ci, v, n, out_rp, out_ci, out_v);
     return cudaGetLastError();
 }
 

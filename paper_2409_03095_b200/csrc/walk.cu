@@ -884,7 +884,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                     keep = rank < kret;
                 }
             }
-            if (keep) {
+            if (keep && !a.unscaled) {
                 v = v / a.t.b1_diag[c];                // scale_columns (mc_engine.cpp:148)
                 keep = !(v == 0.0 && c != rowc);       // prune (mc_engine.cpp:174-176)
             }

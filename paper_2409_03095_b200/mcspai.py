@@ -83,6 +83,8 @@ class McConfig:  # mc_engine.hpp:15-26
     #: host thread each); 0 = env MCMI_GPUS, else 1.  M does not depend on it.
     n_gpus: int = 0
     deg_stats: bool = False  #: also count sum deg(s) over steps (stats["walk_deg_sum"]); ~4% slower
+    #: rows of (I - A)^-1 as estimate_row returns them: no scale_columns, no zero prune
+    unscaled: bool = False
 
     def to_c(self) -> L.mcmi_config:
         c = L.mcmi_config()
@@ -101,7 +103,7 @@ class McConfig:  # mc_engine.hpp:15-26
         c.rng_mode = int(self.rng_mode)
         c.device = int(self.device)
         c.n_gpus = int(self.n_gpus)
-        c.flags = L.MCMI_FLAG_DEG_STATS if self.deg_stats else 0
+        c.flags = (L.MCMI_FLAG_DEG_STATS if self.deg_stats else 0) | (L.MCMI_FLAG_UNSCALED if self.unscaled else 0)
         return c
 
     def oracle_kwargs(self) -> dict:
@@ -310,3 +312,102 @@ def compute_preconditioner_serial(b: CsrMatrix, cfg: McConfig | None = None) -> 
     """The reference's serial twin (mc_engine.hpp:85-86): same contract, so
     the same device build (the result is independent of execution layout)."""
     return compute_preconditioner(b, cfg)
+
+
+# ------------------------------------------------------------ fine-grained API
+# The reference's public building blocks (mc_engine.hpp:55-74, split.hpp:21-39),
+# on the same device code as the build.
+
+def _view(m: CsrMatrix) -> L.mcmi_csr_view:
+    if m.row_ptr.size != m.n + 1:
+        raise ValueError("CsrMatrix arrays are inconsistent with row_ptr")
+    return L.mcmi_csr_view(int(m.n), m.row_ptr.ctypes.data, m.col_idx.ctypes.data if m.col_idx.size else None,
+                           m.values.ctypes.data if m.values.size else None)
+
+
+def derive_chain_budget(cfg: McConfig, a_norm: float) -> ChainBudget:
+    """mcspai::derive_chain_budget (mc_engine.hpp:55): host arithmetic with
+    glibc log/ceil, the code the build itself runs."""
+    c = cfg.to_c()
+    nc, ml = C.c_int64(), C.c_int64()
+    err = C.create_string_buffer(256)
+    raise_for(L.load().mcmi_derive_chain_budget(C.byref(c), float(a_norm), C.byref(nc), C.byref(ml), err, 256),
+              err.value.decode(errors="replace"))
+    return ChainBudget(nc.value, ml.value)
+
+
+@dataclass
+class SplitSystem:  # split.hpp:21-28
+    b_hat: CsrMatrix
+    b1_diag: np.ndarray
+    a: CsrMatrix
+    p: CsrMatrix
+    s_diag: np.ndarray
+    a_norm: float
+    #: (B, alpha, mode) it was derived from: estimate_row rebuilds the device
+    #: tables from these (the device never holds a SplitSystem between calls)
+    source: tuple = field(default=None, repr=False, compare=False)
+
+
+def augment_and_split(b: CsrMatrix, alpha: float, mode: AugmentationMode = AugmentationMode.sign_aware,
+                      device: int = 0) -> SplitSystem:
+    """mcspai::augment_and_split (split.hpp:34-35) on the GPU."""
+    lib = L.load()
+    h = C.c_void_p()
+    err = C.create_string_buffer(512)
+    raise_for(lib.mcmi_augment_and_split(C.byref(_view(b)), float(alpha), int(mode), int(device), C.byref(h), err, 512),
+              err.value.decode(errors="replace"))
+    try:
+        n, nb, na, an = C.c_int64(), C.c_int64(), C.c_int64(), C.c_double()
+        lib.mcmi_split_sizes(h, C.byref(n), C.byref(nb), C.byref(na), C.byref(an))
+        n, nb, na = n.value, nb.value, na.value
+        brp, bci, bv = np.empty(n + 1, np.int64), np.empty(nb, np.int64), np.empty(nb)
+        arp, aci, av, pv = np.empty(n + 1, np.int64), np.empty(na, np.int64), np.empty(na), np.empty(na)
+        b1, sd = np.empty(n), np.empty(n)
+        ptr = lambda x: x.ctypes.data if x.size else None  # noqa: E731
+        lib.mcmi_split_copy(h, ptr(brp), ptr(bci), ptr(bv), ptr(b1), ptr(arp), ptr(aci), ptr(av), ptr(pv), ptr(sd))
+    finally:
+        lib.mcmi_split_free(h)
+    return SplitSystem(CsrMatrix(n, brp, bci, bv), b1, CsrMatrix(n, arp, aci, av), CsrMatrix(n, arp.copy(), aci.copy(), pv),
+                       sd, an.value, source=(b, float(alpha), AugmentationMode(int(mode)), int(device)))
+
+
+def transition_probabilities(a: CsrMatrix, device: int = 0) -> CsrMatrix:
+    """mcspai::transition_probabilities (split.hpp:39) on the GPU."""
+    n, nnz = a.n, int(a.row_ptr[-1]) if a.n > 0 else 0
+    rp, ci, v = np.zeros(n + 1, np.int64), np.empty(nnz, np.int64), np.empty(nnz)
+    k = C.c_int64()
+    err = C.create_string_buffer(512)
+    raise_for(L.load().mcmi_transition_probabilities(C.byref(_view(a)), int(device), rp.ctypes.data,
+                                                     ci.ctypes.data if nnz else None, v.ctypes.data if nnz else None,
+                                                     C.byref(k), err, 512),
+              err.value.decode(errors="replace"))
+    return CsrMatrix(n, rp, ci[: k.value].copy(), v[: k.value].copy())
+
+
+@dataclass
+class RngStream:  # rng.hpp:17-30: RngStream(seed, stream_id)
+    seed: int
+    stream_id: int
+
+
+def estimate_row(split: SplitSystem, r: int, budget: ChainBudget, delta: float, stream: RngStream):
+    """mcspai::estimate_row (mc_engine.hpp:63-65): row r of (I - A)^-1 as
+    (column, value) pairs, column-sorted, from budget.n_chains walks.
+
+    Runs the build's walk kernel on row r with MCMI_FLAG_UNSCALED.  The device
+    keys row r's draws by RngStream(seed, r), the stream compute_preconditioner
+    gives that row (mc_engine.cpp:168); other stream ids are not supported."""
+    if split.source is None:
+        raise ValueError("estimate_row needs a SplitSystem from augment_and_split")
+    if int(stream.stream_id) != int(r):
+        raise ValueError("estimate_row: the device draws row r from RngStream(seed, r); stream_id must equal r")
+    b, alpha, mode, device = split.source
+    if not 0 <= r < b.n:
+        raise IndexError("row out of range")
+    cfg = McConfig(alpha=alpha, mode=mode, delta=float(delta), chains_override=int(budget.n_chains),
+                   max_len_override=int(budget.max_len), master_seed=int(stream.seed), retain_k=0, device=device,
+                   unscaled=True)
+    inv = compute_preconditioner(b, cfg, rows=(int(r), int(r) + 1))
+    return list(zip(inv.m.col_idx.tolist(), inv.m.values.tolist()))
+
