@@ -183,6 +183,13 @@ void mcmi_split_free(mcmi_split_system* s);
 int mcmi_transition_probabilities(const mcmi_csr_view* a, int device, int64_t* p_row_ptr, int64_t* p_col_idx,
                                   double* p_values, int64_t* p_nnz, char* err, size_t errlen);
 
+/* mcspai::drop_small_entries (csr.hpp:76-77, csr.cpp:127-157) on `device`:
+ * the build's drop filter as a matrix.  out_row_ptr[n+1]; out_col_idx /
+ * out_values hold nnz(m) entries; *out_nnz = entries kept.  MCMI_EINVAL:
+ * "drop fraction must lie in [0,1]". */
+int mcmi_drop_small_entries(const mcmi_csr_view* m, double p, int32_t drop_mode, int device, int64_t* out_row_ptr,
+                            int64_t* out_col_idx, double* out_values, int64_t* out_nnz, char* err, size_t errlen);
+
 /* Row blocks of a sharded build: edges[0..parts] with block g =
  * rows [edges[g], edges[g+1]) of [row_begin, row_end), balanced on cost(r) =
  * 1 + nnz(r); edges[g] (0 < g < parts) is the first row whose cost prefix

@@ -24,7 +24,7 @@ EXPORTS = [
     "mcmi_host_register", "mcmi_host_unregister", "mcmi_from_triplets", "mcmi_mm_parse", "mcmi_mm_read_file",
     "mcmi_host_csr_get", "mcmi_host_csr_free", "mcmi_mm_format", "mcmi_mm_write_file", "mcmi_recover_inverse",
     "mcmi_recover_inverse_device", "mcmi_scatter_shard", "mcmi_derive_chain_budget", "mcmi_augment_and_split",
-    "mcmi_split_sizes", "mcmi_split_copy", "mcmi_split_free", "mcmi_transition_probabilities",
+    "mcmi_split_sizes", "mcmi_split_copy", "mcmi_split_free", "mcmi_transition_probabilities", "mcmi_drop_small_entries",
 ]
 
 
@@ -135,6 +135,8 @@ def load(path: str | None = None):
     L.mcmi_split_copy.argtypes = [C.c_void_p] + [C.c_void_p] * 9
     L.mcmi_split_free.argtypes = [C.c_void_p]
     L.mcmi_split_free.restype = None
+    L.mcmi_drop_small_entries.argtypes = [C.c_void_p, C.c_double, C.c_int32, C.c_int, C.c_void_p, C.c_void_p,
+                                          C.c_void_p, _i64p, C.c_char_p, C.c_size_t]
     L.mcmi_transition_probabilities.argtypes = [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, _i64p,
                                                 C.c_char_p, C.c_size_t]
     L.mcmi_result_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,

@@ -1202,6 +1202,54 @@ Status augment_and_split_dev(mcmi_engine* e, const mcmi_csr_view& b, double alph
     return ok();
 }
 
+Status drop_small_entries_dev(mcmi_engine* e, const mcmi_csr_view& m, double p, int drop_mode, int64_t* o_rp,
+                              int64_t* o_ci, double* o_v, int64_t* o_nnz) {
+    if (!(p >= 0.0 && p <= 1.0)) return fail(MCMI_EINVAL, "drop fraction must lie in [0,1]");  // csr.cpp:128-129
+    MCMI_TRY(cudaSetDevice(e->device), "cudaSetDevice");
+    cudaStream_t s = e->own;
+    DevTemps t(s);
+    mcmi_csr_view dv{};
+    if (Status st = stage_csr(e, m, t, &dv); st.code) return st;
+    const int64_t n = m.n, nnz = n > 0 ? m.row_ptr[n] : 0;
+    TableBuildArgs ta{};
+    ta.n = n;
+    ta.row_ptr = dv.row_ptr;
+    ta.col_idx = dv.col_idx;
+    ta.values = dv.values;
+    ta.drop_fraction = p;
+    ta.drop_mode = drop_mode;
+    ta.red = e->red.as<Reductions>();
+    const bool active = p != 0.0 && n > 0;
+    if (active && drop_mode == MCMI_DROP_COUNT_QUANTILE) {
+        MCMI_TRY(e->keep.ensure(std::max<int64_t>(nnz, 1)), "alloc keep");
+        MCMI_TRY(e->cq_tmp.ensure(count_quantile_scratch_bytes(std::max<int64_t>(nnz, 1))), "alloc cq");
+        ta.keep = e->keep.as<unsigned char>();
+        MCMI_TRY(launch_count_quantile(ta, nnz, 0, e->cq_tmp.p, e->cq_tmp.cap, s), "count-quantile drop");
+    }
+    int* cnt = t.get<int>(n);
+    int64_t* orp = t.get<int64_t>(n + 1);
+    MCMI_TRY(t.err, "alloc");
+    MCMI_TRY(e->scan_tmp.ensure(scan_scratch_bytes(std::max<int64_t>(n, 1)) + 64), "alloc scan");
+    MCMI_TRY(launch_drop_filter(ta, active, 0, cnt, nullptr, nullptr, nullptr, s), "drop count");
+    MCMI_TRY(scan_rows_exclusive(cnt, orp, n, e->scan_tmp.p, s), "scan");
+    int64_t tot = 0;
+    if (n > 0) MCMI_TRY(cudaMemcpyAsync(&tot, orp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+    MCMI_TRY(cudaStreamSynchronize(s), "scan");
+    int64_t* oci = t.get<int64_t>(tot);
+    double* ov = t.get<double>(tot);
+    MCMI_TRY(t.err, "alloc");
+    MCMI_TRY(launch_drop_filter(ta, active, 1, nullptr, orp, oci, ov, s), "drop fill");
+    if (n > 0) MCMI_TRY(cudaMemcpyAsync(o_rp, orp, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+    if (tot) {
+        MCMI_TRY(cudaMemcpyAsync(o_ci, oci, tot * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+        MCMI_TRY(cudaMemcpyAsync(o_v, ov, tot * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    }
+    MCMI_TRY(cudaStreamSynchronize(s), "D2H");
+    if (n == 0) o_rp[0] = 0;
+    *o_nnz = tot;
+    return ok();
+}
+
 Status transition_probabilities_dev(mcmi_engine* e, const mcmi_csr_view& a, int64_t* p_rp, int64_t* p_ci,
                                     double* p_v, int64_t* p_nnz) {
     MCMI_TRY(cudaSetDevice(e->device), "cudaSetDevice");
@@ -1412,6 +1460,21 @@ int mcmi_transition_probabilities(const mcmi_csr_view* a, int device, int64_t* p
     mcmi_engine* e = acquire_engine(device, &st);
     if (!e) return report(st, err, errlen);
     st = transition_probabilities_dev(e, *a, p_row_ptr, p_col_idx, p_values, p_nnz);
+    release_engine(e);
+    return report(st, err, errlen);
+}
+
+int mcmi_drop_small_entries(const mcmi_csr_view* m, double p, int32_t drop_mode, int device, int64_t* out_row_ptr,
+                            int64_t* out_col_idx, double* out_values, int64_t* out_nnz, char* err, size_t errlen) {
+    const mcmi::DeviceGuard device_guard;
+    if (!out_row_ptr || !out_nnz) return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    if (Status st = check_host_view(m); st.code) return report(st, err, errlen);
+    if (m->n > 0 && m->row_ptr[m->n] > 0 && (!out_col_idx || !out_values))
+        return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    Status st;
+    mcmi_engine* e = acquire_engine(device, &st);
+    if (!e) return report(st, err, errlen);
+    st = drop_small_entries_dev(e, *m, p, drop_mode, out_row_ptr, out_col_idx, out_values, out_nnz);
     release_engine(e);
     return report(st, err, errlen);
 }

@@ -149,6 +149,9 @@ cudaError_t launch_validate_row_ptr(const int64_t* row_ptr, int64_t n, int64_t n
 cudaError_t launch_table_build(const TableBuildArgs& a, int64_t nnz, bool drop_active,
                                cudaStream_t s);
 cudaError_t launch_table_fill(const TableBuildArgs& a, cudaStream_t s);
+// drop_small_entries: pass 0 row counts (value range first), pass 1 fill.
+cudaError_t launch_drop_filter(const TableBuildArgs& a, bool drop_active, int pass, int* cnt, const int64_t* out_rp,
+                               int64_t* oci, double* ov, cudaStream_t s);
 // pass 0: norms, diagonal, row counts, ||A||; pass 1: fill b_hat / A / P.
 cudaError_t launch_split_export(const SplitExportArgs& a, int pass, cudaStream_t s);
 // pass 0: row counts into cnt; pass 1: fill with out_rp (exclusive scan of cnt).

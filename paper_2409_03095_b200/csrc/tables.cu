@@ -533,6 +533,34 @@ __global__ void k_tp_fill(const int64_t* __restrict__ rp, const int64_t* __restr
         }
     }
 }
+
+// drop_small_entries as a matrix (mcmi_drop_small_entries): the build's keep
+// predicate, then filter_entries (csr.cpp:109-123) in stored order.
+__global__ void k_drop_count(TableBuildArgs a, int* __restrict__ cnt) {
+    const Keep keep = make_keep(a);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int c = 0;
+        for (int64_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) c += keep(i, k, a.col_idx[k], a.values[k]) ? 1 : 0;
+        cnt[i] = c;
+    }
+}
+
+__global__ void k_drop_fill(TableBuildArgs a, const int64_t* __restrict__ out_rp, int64_t* __restrict__ oci,
+                            double* __restrict__ ov) {
+    const Keep keep = make_keep(a);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t o = out_rp[i];
+        for (int64_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) {
+            const int64_t c = a.col_idx[k];
+            const double v = a.values[k];
+            if (!keep(i, k, c, v)) continue;
+            oci[o] = c;
+            ov[o++] = v;
+        }
+    }
+}
 }  // namespace
 
 size_t count_quantile_scratch_bytes(int64_t nnz) {
@@ -608,6 +636,19 @@ cudaError_t launch_transition_probabilities(const int64_t* rp, const int64_t* ci
     if (n <= 0) return cudaSuccess;
     if (pass == 0) k_tp_count<<<grid_for(n), TB, 0, s>>>(rp, v, n, cnt);
     else k_tp_fill<<<grid_for(n), TB, 0, s>>>(rp, ci, v, n, out_rp, out_ci, out_v);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_drop_filter(const TableBuildArgs& a, bool drop_active, int pass, int* cnt, const int64_t* out_rp,
+                               int64_t* oci, double* ov, cudaStream_t s) {
+    if (a.n <= 0) return cudaSuccess;
+    const int g = grid_for(a.n);
+    if (pass == 0) {
+        if (drop_active && a.drop_mode == 0) k_offdiag_range<<<g, TB, 0, s>>>(a);
+        k_drop_count<<<g, TB, 0, s>>>(a, cnt);
+    } else {
+        k_drop_fill<<<g, TB, 0, s>>>(a, out_rp, oci, ov);
+    }
     return cudaGetLastError();
 }
 

@@ -385,6 +385,20 @@ def transition_probabilities(a: CsrMatrix, device: int = 0) -> CsrMatrix:
     return CsrMatrix(n, rp, ci[: k.value].copy(), v[: k.value].copy())
 
 
+def drop_small_entries(m: CsrMatrix, p: float, mode: DropMode = DropMode.value_range, device: int = 0) -> CsrMatrix:
+    """mcspai::drop_small_entries (csr.hpp:76-77) on the GPU: the build's drop
+    filter (value range or count quantile, diagonal never dropped)."""
+    n, nnz = m.n, int(m.row_ptr[-1]) if m.n > 0 else 0
+    rp, ci, v = np.zeros(n + 1, np.int64), np.empty(nnz, np.int64), np.empty(nnz)
+    k = C.c_int64()
+    err = C.create_string_buffer(512)
+    raise_for(L.load().mcmi_drop_small_entries(C.byref(_view(m)), float(p), int(mode), int(device), rp.ctypes.data,
+                                               ci.ctypes.data if nnz else None, v.ctypes.data if nnz else None,
+                                               C.byref(k), err, 512),
+              err.value.decode(errors="replace"))
+    return CsrMatrix(n, rp, ci[: k.value].copy(), v[: k.value].copy())
+
+
 @dataclass
 class RngStream:  # rng.hpp:17-30: RngStream(seed, stream_id)
     seed: int

@@ -171,3 +171,34 @@ def test_estimate_row_rejects_other_streams():
     sp = augment_and_split(G.convection_diffusion(10), 5.0)
     with pytest.raises(ValueError, match="stream_id must equal r"):
         estimate_row(sp, 3, ChainBudget(10, 2), 0.1, RngStream(0, 4))
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["convdiff20", "powerlaw500", "ragged60", "dupdiag"])
+@pytest.mark.parametrize("p", [0.0, 0.1, 0.5, 0.999, 1.0])
+@pytest.mark.parametrize("mode", [0, 1])
+def test_drop_small_entries_matches_reference(ref_mod, name, p, mode):
+    from paper_2409_03095_b200.mcspai import drop_small_entries
+    b = _matrices()[name]
+    _same_csr(drop_small_entries(b, p, mode), ref_mod.drop_small_entries(_ref_csr(ref_mod, b), p, mode))
+
+
+@pytest.mark.gpu
+def test_drop_small_entries_ties_and_errors(ref_mod):
+    """Equal magnitudes (count quantile breaks ties by position) and the
+    reference's range error."""
+    from paper_2409_03095_b200.mcspai import CsrMatrix, drop_small_entries
+    n = 40
+    rng = np.random.default_rng(1)
+    rp = np.arange(0, 4 * n + 1, 4)
+    ci = np.array([[i, (i + 1) % n, (i + 2) % n, (i + 5) % n] for i in range(n)]).ravel()
+    order = np.argsort(ci.reshape(n, 4), axis=1)
+    ci = np.take_along_axis(ci.reshape(n, 4), order, axis=1).ravel()
+    v = rng.choice([-0.5, 0.5, 0.25, 1.0], size=4 * n)
+    b = CsrMatrix(n, rp, ci, v)
+    for p in (0.2, 0.37, 0.75):
+        for mode in (0, 1):
+            _same_csr(drop_small_entries(b, p, mode), ref_mod.drop_small_entries(_ref_csr(ref_mod, b), p, mode))
+    for bad in (-0.1, 1.1, float("nan")):
+        with pytest.raises(ValueError, match=r"^drop fraction must lie in \[0,1\]$"):
+            drop_small_entries(b, bad)
