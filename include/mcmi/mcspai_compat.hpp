@@ -225,6 +225,95 @@ DenseT recover_inverse(const DenseT& b_hat_inv, const PlanT& plan, double tol = 
     return out;
 }
 
+// ---- fine-grained building blocks on the reference's types
+
+template <class ChainBudgetT, class CfgT>
+ChainBudgetT derive_chain_budget(const CfgT& cfg, double a_norm) {  // mc_engine.hpp:55
+    const mcmi_config c = to_config(cfg, Options{});
+    char err[256] = {0};
+    int64_t nc = 0, ml = 0;
+    const int code = mcmi_derive_chain_budget(&c, a_norm, &nc, &ml, err, sizeof err);
+    if (code != MCMI_OK) rethrow<std::runtime_error>(code, err);
+    ChainBudgetT b;
+    b.n_chains = nc;
+    b.max_len = ml;
+    return b;
+}
+
+template <class CsrT, class ModeT>
+CsrT drop_small_entries(const CsrT& m, double p, ModeT mode, const Options& opt = {}) {  // csr.hpp:76-77
+    const mcmi_csr_view v = detail::view_of(m);
+    CsrT out;
+    out.n = m.n;
+    out.row_ptr.resize(static_cast<size_t>(m.n) + 1);
+    out.col_idx.resize(m.col_idx.size());
+    out.values.resize(m.values.size());
+    char err[512] = {0};
+    int64_t nnz = 0;
+    const int code = mcmi_drop_small_entries(&v, p, static_cast<int32_t>(mode), opt.device,
+                                             reinterpret_cast<int64_t*>(out.row_ptr.data()),
+                                             reinterpret_cast<int64_t*>(out.col_idx.data()), out.values.data(), &nnz,
+                                             err, sizeof err);
+    if (code != MCMI_OK) rethrow<std::runtime_error>(code, err);
+    out.col_idx.resize(static_cast<size_t>(nnz));
+    out.values.resize(static_cast<size_t>(nnz));
+    return out;
+}
+
+template <class CsrT>
+CsrT transition_probabilities(const CsrT& a, const Options& opt = {}) {  // split.hpp:39
+    const mcmi_csr_view v = detail::view_of(a);
+    CsrT out;
+    out.n = a.n;
+    out.row_ptr.resize(static_cast<size_t>(a.n) + 1);
+    out.col_idx.resize(a.col_idx.size());
+    out.values.resize(a.values.size());
+    char err[512] = {0};
+    int64_t nnz = 0;
+    const int code = mcmi_transition_probabilities(&v, opt.device, reinterpret_cast<int64_t*>(out.row_ptr.data()),
+                                                   reinterpret_cast<int64_t*>(out.col_idx.data()), out.values.data(),
+                                                   &nnz, err, sizeof err);
+    if (code != MCMI_OK) rethrow<std::runtime_error>(code, err);
+    out.col_idx.resize(static_cast<size_t>(nnz));
+    out.values.resize(static_cast<size_t>(nnz));
+    return out;
+}
+
+template <class SplitSystemT, class SplitErrorT, class CsrT, class ModeT>
+SplitSystemT augment_and_split(const CsrT& b, double alpha, ModeT mode, const Options& opt = {}) {  // split.hpp:34-35
+    const mcmi_csr_view v = detail::view_of(b);
+    char err[512] = {0};
+    mcmi_split_system* h = nullptr;
+    const int code = mcmi_augment_and_split(&v, alpha, static_cast<int32_t>(mode), opt.device, &h, err, sizeof err);
+    if (code != MCMI_OK) rethrow<SplitErrorT>(code, err);
+    struct Guard {
+        mcmi_split_system* h;
+        ~Guard() { mcmi_split_free(h); }
+    } guard{h};
+    int64_t n = 0, nb = 0, na = 0;
+    double a_norm = 0.0;
+    mcmi_split_sizes(h, &n, &nb, &na, &a_norm);
+    SplitSystemT s;
+    s.b_hat.n = s.a.n = s.p.n = n;
+    s.b_hat.row_ptr.resize(static_cast<size_t>(n) + 1);
+    s.b_hat.col_idx.resize(static_cast<size_t>(nb));
+    s.b_hat.values.resize(static_cast<size_t>(nb));
+    s.a.row_ptr.resize(static_cast<size_t>(n) + 1);
+    s.a.col_idx.resize(static_cast<size_t>(na));
+    s.a.values.resize(static_cast<size_t>(na));
+    s.p.values.resize(static_cast<size_t>(na));
+    s.b1_diag.resize(static_cast<size_t>(n));
+    s.s_diag.resize(static_cast<size_t>(n));
+    mcmi_split_copy(h, reinterpret_cast<int64_t*>(s.b_hat.row_ptr.data()),
+                    reinterpret_cast<int64_t*>(s.b_hat.col_idx.data()), s.b_hat.values.data(), s.b1_diag.data(),
+                    reinterpret_cast<int64_t*>(s.a.row_ptr.data()), reinterpret_cast<int64_t*>(s.a.col_idx.data()),
+                    s.a.values.data(), s.p.values.data(), s.s_diag.data());
+    s.p.row_ptr = s.a.row_ptr;  // P has A's pattern (A holds no zeros)
+    s.p.col_idx = s.a.col_idx;
+    s.a_norm = a_norm;
+    return s;
+}
+
 }  // namespace compat
 }  // namespace mcmi
 

@@ -124,5 +124,29 @@ int main(int argc, char** argv) {
         std::printf("[%s] recover_inverse n=%lld bit-identical\n", same ? "PASS" : "FAIL", static_cast<long long>(b.n));
         ok &= same;
     }
+    // the fine-grained building blocks against the reference's own
+    {
+        const CsrMatrix b = make_random_ddm(300, 0.05, 11);
+        bool same = true;
+        for (const auto mode : {AugmentationMode::sign_aware, AugmentationMode::plain}) {
+            const SplitSystem r = augment_and_split(b, 1.5, mode);
+            const SplitSystem g = mcmi::compat::augment_and_split<SplitSystem, SplitError>(b, 1.5, mode);
+            same &= r.b_hat == g.b_hat && r.a == g.a && r.p == g.p && r.b1_diag == g.b1_diag &&
+                    r.s_diag == g.s_diag && r.a_norm == g.a_norm;
+            same &= mcmi::compat::transition_probabilities(r.a) == transition_probabilities(r.a);
+        }
+        for (const auto dm : {DropMode::value_range, DropMode::count_quantile})
+            for (const double p : {0.0, 0.2, 0.7})
+                same &= mcmi::compat::drop_small_entries(b, p, dm) == drop_small_entries(b, p, dm);
+        McConfig c;
+        for (const double a : {0.0, 0.1, 0.5, 0.95}) {
+            const ChainBudget r = derive_chain_budget(c, a);
+            const ChainBudget g = mcmi::compat::derive_chain_budget<ChainBudget>(c, a);
+            same &= r.n_chains == g.n_chains && r.max_len == g.max_len;
+        }
+        std::printf("[%s] augment_and_split / transition_probabilities / drop_small_entries / derive_chain_budget "
+                    "bit-identical\n", same ? "PASS" : "FAIL");
+        ok &= same;
+    }
     return ok ? 0 : 1;
 }
