@@ -420,8 +420,21 @@ __device__ int sort_by_column(int* keys, double* vals, int s) {
 
 constexpr int kRankTopkMax = 256;  // above this row length retain_top_k uses radix_topk
 
-template <int MODE, int MINB, bool GL, bool DEG, int LF = 0, int CAPC = 0>
+// Neighbourhood slot tables (NB variant, L = 2 with the 256-slot tier): at row
+// start the warp inserts r's columns and its neighbours' columns into the hash
+// once and keeps T1[i] = slot of r's i-th column, T2[off[i] + j] = slot of the
+// j-th column of r's i-th neighbour.  A step then logs a slot instead of a
+// column (equal slots <=> equal columns, so the (chain, step) fold order is
+// unchanged), the fold needs no hash probe, and the last step needs no column
+// load.  A touched-slot mask keeps the emitted set = the visited columns.
+// Rows whose neighbourhood exceeds the tables or the tier run the plain path.
+constexpr int kNbDeg = 32;    // max deg(r)
+constexpr int kNbT2 = 704;    // max sum of the neighbours' degrees
+constexpr int kNbBytes = 32 + 2 * kNbDeg + kNbDeg + kNbT2;  // mask[8] u32, off[32] u16, T1[32] u8, T2 u8
+
+template <int MODE, int MINB, bool GL, bool DEG, int LF = 0, int CAPC = 0, bool NB = false>
 __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
+    static_assert(!NB || (LF == 2 && CAPC == 256 && !GL), "NB: L = 2 kernel, 256-slot shared tier");
     // LF > 0: a launch with max_len == log_stride == LF and 32-lane batches:
     // the step loop (unrolled, no length or log-capacity tests) and the fold's
     // position arithmetic are compile-time.
@@ -436,12 +449,17 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     const int S = LF ? LF : a.log_stride;       // step deposits per chain (max_len)
     const int B = LF ? 32 : a.lanes;            // chains per batch
     const int logn = LF ? round32(32 * LF) : a.log_n;  // round32(B * S), host-computed (kernel parameter)
-    const size_t per_warp = (LF && CAPC) ? static_cast<size_t>(CAPC + logn) * 12  // walk_smem_bytes_per_warp
+    const size_t per_warp = (LF && CAPC) ? static_cast<size_t>(CAPC + logn) * 12 + (NB ? kNbBytes : 0)
                                          : static_cast<size_t>(a.warp_bytes);
     // GL: per-warp accumulator + log in global scratch (large rows / long walks)
     unsigned char* wbase = GL ? a.gscratch + per_warp * (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp)
                               : smem_raw + per_warp * warp;
     const WarpSmem sm = carve(wbase, cap, logn);
+    // NB tables after the log (per_warp - kNbBytes)
+    unsigned* const nb_mask = NB ? reinterpret_cast<unsigned*>(wbase + (per_warp - kNbBytes)) : nullptr;
+    unsigned short* const nb_off = NB ? reinterpret_cast<unsigned short*>(nb_mask + 8) : nullptr;
+    unsigned char* const nb_t1 = NB ? reinterpret_cast<unsigned char*>(nb_off + kNbDeg) : nullptr;
+    unsigned char* const nb_t2 = NB ? nb_t1 + kNbDeg : nullptr;
     const unsigned cap_mask = static_cast<unsigned>(cap - 1);
     const int shift = CAPC ? 32 - (31 - __clz(CAPC)) : a.hash_shift;  // 32 - log2(cap)
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -478,6 +496,66 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
         if (lane == 0) slot_r = hash_slot<GL>(sm.keys, cap_mask, shift, rowc, n_new0);
         slot_r = __shfl_sync(FULL_MASK, slot_r, 0);
         double acc_r = 0.0;
+
+        bool nb = false;  // NB: this row logs slots (warp-uniform)
+        if (NB) {
+            __syncwarp();
+            uint4 q0, q1;
+            ldg256(rec + 2 * static_cast<int64_t>(rowc), q0, q1);
+            const unsigned dr = q0.y;
+            if (dr <= static_cast<unsigned>(kNbDeg)) {
+                unsigned da = 0, ba = 0;
+                int ca = 0;
+                if (static_cast<unsigned>(lane) < dr) {
+                    ca = tcol[q0.x + lane];
+                    uint4 p0, p1;
+                    ldg256(rec + 2 * static_cast<int64_t>(ca), p0, p1);
+                    da = p0.y;
+                    ba = p0.x;
+                }
+                unsigned incl = da;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const unsigned nbv = __shfl_up_sync(FULL_MASK, incl, o);
+                    if (lane >= o) incl += nbv;
+                }
+                const unsigned tot = __shfl_sync(FULL_MASK, incl, 31);
+                if (tot <= static_cast<unsigned>(kNbT2)) {
+                    const unsigned offa = incl - da;
+                    int nn = 0;
+                    bool bad = false;
+                    if (static_cast<unsigned>(lane) < dr) {
+                        nb_off[lane] = static_cast<unsigned short>(offa);
+                        const int sl = hash_slot<false>(sm.keys, cap_mask, shift, ca, nn);
+                        if (sl < 0) bad = true;
+                        else nb_t1[lane] = static_cast<unsigned char>(sl);
+                    }
+                    __syncwarp();
+                    for (unsigned i = 0; i < dr; ++i) {
+                        const unsigned di = __shfl_sync(FULL_MASK, da, i);
+                        const unsigned bi = __shfl_sync(FULL_MASK, ba, i);
+                        const unsigned oi = __shfl_sync(FULL_MASK, offa, i);
+                        for (unsigned j = lane; j < di; j += 32) {
+                            const int sl = hash_slot<false>(sm.keys, cap_mask, shift, tcol[bi + j], nn);
+                            if (sl < 0) bad = true;
+                            else nb_t2[oi + j] = static_cast<unsigned char>(sl);
+                        }
+                        __syncwarp();
+                    }
+                    const int pre = 1 + warp_sum_int(nn);
+                    nb = !__any_sync(FULL_MASK, bad) && pre <= CAPC - CAPC / 4;
+                    if (!nb) {  // does not fit: back to an accumulator holding only r
+                        for (int i = lane; i < cap; i += 32) sm.keys[i] = EMPTY_KEY;
+                        __syncwarp();
+                        if (lane == 0) slot_r = hash_slot<false>(sm.keys, cap_mask, shift, rowc, n_new0);
+                        slot_r = __shfl_sync(FULL_MASK, slot_r, 0);
+                    }
+                }
+            }
+            if (nb && lane < 8) nb_mask[lane] = lane == (slot_r >> 5) ? (1u << (slot_r & 31)) : 0u;
+            __syncwarp();
+        }
+        const int rkey = (NB && nb) ? slot_r : rowc;  // log key of column r
 
         int distinct = 1;
         bool overflow = false;
@@ -517,6 +595,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             uint4 blk = make_uint4(0, 0, 0, 0);
             bool alive = active;
             bool log_full = false;  // the walk would outgrow this tier's deposit log
+            unsigned nb_i1 = 0;     // NB: entry index of the first step in row r
 #pragma unroll
             for (int t = 0; LF ? (t < LF) : __any_sync(FULL_MASK, alive); ++t) {
                 if (LF) {  // compile-time trip count: no log overflow, no length test
@@ -539,7 +618,8 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 ++lane_steps;
                 if (DEG) lane_deg += deg;
                 double ratio;
-                int nxt;
+                int nxt = 0;
+                unsigned kidx = 0;  // entry index within the state's row (NB)
                 if (deg == 1) {  // forced move, no draw (mc_engine.cpp:69); inline in the record
                     ratio = __hiloint2double(static_cast<int>(r0.w), static_cast<int>(r0.z));
                     nxt = static_cast<int>(r1.z);
@@ -601,14 +681,27 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                         }
                     }
                     if (!found) ratio = ent[end - 1].y;
-                    nxt = tcol[k];
+                    kidx = k - r0.x;
+                    if (!(NB && nb && t == 1)) nxt = tcol[k];  // NB: the last step logs a slot only
                 }
                 w *= ratio;  // w *= a_k / p_k (mc_engine.cpp:94)
-                state = nxt;
-                lc[m * B] = state;
+                int logv;
+                if (NB && nb) {
+                    if (t == 0) {
+                        nb_i1 = kidx;
+                        logv = nb_t1[kidx];
+                    } else {
+                        logv = nb_t2[nb_off[nb_i1] + kidx];
+                    }
+                    state = nxt;
+                } else {
+                    state = nxt;
+                    logv = state;
+                }
+                lc[m * B] = logv;
                 lw[m * B] = w;
                 ++m;
-                if (state == rowc) {
+                if (logv == rkey) {
                     if (retm == 0 && !ret_hi) ret_w = w;
                     if (m <= 32) retm |= 1u << (m - 1);
                     else ret_hi = true;
@@ -743,7 +836,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 bool ok = p < span && ((valid >> j) & 1u);
                 const int q = (p - j * S) * B + j;  // chain-major position p -> step-major slot
                 int c = ok ? sm.log_col[q] : -1;
-                ok = ok && c >= 0 && c != rowc;  // column r was folded in (i)
+                ok = ok && c >= 0 && c != rkey;  // column r was folded in (i)
                 if (!ok) c = -1 - lane;          // unique non-column tag
                 const unsigned peers = __match_any_sync(FULL_MASK, c);
                 // group rank = position of this entry among equal columns of the
@@ -756,8 +849,13 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 const int leader = __ffs(peers) - 1;
                 int slot = 0;
                 if (ok && rank == 0) {
-                    slot = hash_slot<GL>(sm.keys, cap_mask, shift, c, n_new);
-                    if (slot < 0) fail = true;
+                    if (NB && nb) {
+                        slot = c;
+                        atomicOr(&nb_mask[c >> 5], 1u << (c & 31));
+                    } else {
+                        slot = hash_slot<GL>(sm.keys, cap_mask, shift, c, n_new);
+                        if (slot < 0) fail = true;
+                    }
                 }
                 slot = __shfl_sync(FULL_MASK, slot, leader);
                 const double w = ok ? sm.log_w[q] : 0.0;
@@ -796,6 +894,11 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
         tot_steps += row_steps;
         tot_deg += row_deg;
         if (lane == 0) sm.vals[slot_r] = acc_r;
+        unsigned nb_bits = 0;  // NB: lane l < 8 holds touched-mask word l
+        if (NB && nb) {
+            nb_bits = lane < 8 ? nb_mask[lane] : 0u;
+            distinct = warp_sum_int(__popc(nb_bits));
+        }
         __syncwarp();
 
         // ------------------------------------------------------ finalize
@@ -805,11 +908,17 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             const int i = i0 + lane;
             const int kk = sm.keys[i];
             const double vv = sm.vals[i];
-            const bool occ = kk != EMPTY_KEY;
+            bool occ = kk != EMPTY_KEY;
+            bool drop = false;  // NB: pre-inserted but never visited
+            if (NB && nb) {
+                const unsigned wbits = __shfl_sync(FULL_MASK, nb_bits, i0 >> 5);
+                drop = occ && !((wbits >> lane) & 1u);
+                occ = occ && !drop;
+            }
             const unsigned bal = __ballot_sync(FULL_MASK, occ);
             const int dst = o + __popc(bal & lt_mask);
             __syncwarp();
-            if (occ && dst != i) {
+            if ((occ && dst != i) || drop) {
                 sm.keys[i] = EMPTY_KEY;
                 sm.vals[i] = 0.0;
             }
@@ -928,16 +1037,17 @@ size_t walk_global_bytes_per_warp(int cap, int lanes, int log_stride) {
     return walk_smem_bytes_per_warp(cap, lanes, log_stride);
 }
 
-template <int MODE, int MINB, bool GL, bool DEG, int LF = 0, int CAPC = 0>
+template <int MODE, int MINB, bool GL, bool DEG, int LF = 0, int CAPC = 0, bool NB = false>
 cudaError_t launch_walk_t(const WalkArgs& a, int warps_per_block, int num_sms, int64_t max_warps,
                           cudaStream_t s) {
-    const size_t smem = GL ? 0 : walk_smem_bytes_per_warp(a.cap, a.lanes, a.log_stride) * warps_per_block;
+    const size_t smem =
+        GL ? 0 : (walk_smem_bytes_per_warp(a.cap, a.lanes, a.log_stride) + (NB ? kNbBytes : 0)) * warps_per_block;
     const int threads = warps_per_block * 32;
-    cudaError_t e = cudaFuncSetAttribute(k_walk<MODE, MINB, GL, DEG, LF, CAPC>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaError_t e = cudaFuncSetAttribute(k_walk<MODE, MINB, GL, DEG, LF, CAPC, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
     if (e != cudaSuccess) return e;
     int per_sm = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<MODE, MINB, GL, DEG, LF, CAPC>, threads, smem);
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_walk<MODE, MINB, GL, DEG, LF, CAPC, NB>, threads, smem);
     if (e != cudaSuccess) return e;
     if (per_sm < 1) return cudaErrorInvalidConfiguration;
     int64_t blocks = static_cast<int64_t>(per_sm) * num_sms;
@@ -945,7 +1055,7 @@ cudaError_t launch_walk_t(const WalkArgs& a, int warps_per_block, int num_sms, i
     if (blocks > need) blocks = need;
     if (max_warps > 0 && blocks * warps_per_block > max_warps)
         blocks = std::max<int64_t>(1, max_warps / warps_per_block);
-    k_walk<MODE, MINB, GL, DEG, LF, CAPC><<<static_cast<unsigned>(blocks), threads, smem, s>>>(a);
+    k_walk<MODE, MINB, GL, DEG, LF, CAPC, NB><<<static_cast<unsigned>(blocks), threads, smem, s>>>(a);
     return cudaGetLastError();
 }
 
@@ -960,6 +1070,13 @@ int walk_minb() {
     return v;
 }
 
+// MCMI_WALK_NB=0 (env, tuning and tests) disables the neighbourhood slot
+// tables of the L = 2 / 256-slot kernel.
+bool walk_nb() {
+    const char* e = getenv("MCMI_WALK_NB");
+    return !(e && e[0] == '0');
+}
+
 // The compile-time (walk length, capacity) variants of k_walk for MODE 0 / 1;
 // false if none fits this launch (lanes must be 32 and log_stride == L).
 template <int MODE>
@@ -969,7 +1086,8 @@ bool launch_specialised(const WalkArgs& a, int wpb, int sms, cudaStream_t s, cud
         case 2:
             *err = a.cap == 32    ? launch_walk_t<MODE, 6, false, false, 2, 32>(a, wpb, sms, 0, s)
                    : a.cap == 64  ? launch_walk_t<MODE, 6, false, false, 2, 64>(a, wpb, sms, 0, s)
-                   : a.cap == 256 ? launch_walk_t<MODE, 6, false, false, 2, 256>(a, wpb, sms, 0, s)
+                   : a.cap == 256 ? (walk_nb() ? launch_walk_t<MODE, 6, false, false, 2, 256, true>(a, wpb, sms, 0, s)
+                                               : launch_walk_t<MODE, 6, false, false, 2, 256>(a, wpb, sms, 0, s))
                                   : launch_walk_t<MODE, 6, false, false, 2>(a, wpb, sms, 0, s);
             return true;
         case 3:

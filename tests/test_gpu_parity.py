@@ -417,3 +417,35 @@ def test_walk_length_specialisations_match_generic(mc, oracle_mod, rng, max_len)
                                              **cfg.oracle_kwargs())
     nnz = int(spec.m.row_ptr[300])
     assert np.array_equal(spec.m.col_idx[:nnz], want.col_idx) and bits_equal(spec.m.values[:nnz], want.values)
+
+
+@pytest.mark.parametrize("rng", [0, 1])
+@pytest.mark.parametrize("over", [{}, {"epsilon": 0.02, "delta": 0.01}, {"retain_k": 20, "master_seed": 3},
+                                  {"chains_override": 77, "max_len_override": 2, "delta": 0.2}])
+def test_neighbourhood_slot_tables_match_plain_kernel(mc, oracle_mod, rng, over):
+    """The L = 2 / 256-slot kernel with neighbourhood slot tables (default)
+    equals the plain kernel (MCMI_WALK_NB=0) bit for bit, RowMeta included, and
+    the oracle on sampled rows.  stencil27 interiors use the tables (deg 26,
+    125 two-hop columns); the boundary rows and delta=0.2 (chains that stop
+    after one step) cover mixed and unvisited neighbourhood columns."""
+    import os
+    from paper_2409_03095_b200 import generators as G
+    b = G.stencil27(14, 13, 12, seed=4)
+    cfg = mc.McConfig(rng_mode=rng, **over)
+    nbk = mc.compute_preconditioner(b, cfg)
+    assert nbk.stats["hash_cap"] == 256 and nbk.budget_echo.max_len == 2
+    os.environ["MCMI_WALK_NB"] = "0"
+    try:
+        plain = mc.compute_preconditioner(b, cfg)
+    finally:
+        del os.environ["MCMI_WALK_NB"]
+    assert nbk.m == plain.m and nbk.stats["walk_steps"] == plain.stats["walk_steps"]
+    assert np.array_equal(nbk.row_meta.entries_before_retention, plain.row_meta.entries_before_retention)
+    assert np.array_equal(nbk.row_meta.chains_used, plain.row_meta.chains_used)
+    n = b.n
+    for lo, hi in [(0, 40), (n // 2, n // 2 + 40)]:
+        want = oracle_mod.compute_preconditioner(n, b.row_ptr, b.col_idx, b.values, row_begin=lo, row_end=hi,
+                                                 **cfg.oracle_kwargs())
+        a, z = nbk.m.row_ptr[lo], nbk.m.row_ptr[hi]
+        assert np.array_equal(nbk.m.col_idx[a:z], want.col_idx) and bits_equal(nbk.m.values[a:z], want.values)
+        assert np.array_equal(nbk.row_meta.entries_before_retention[lo:hi], want.entries_before)
