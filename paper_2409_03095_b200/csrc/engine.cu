@@ -492,6 +492,12 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         wa.ell0 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(L, 2)));
         wa.deg_stats = (cfg.flags & MCMI_FLAG_DEG_STATS) ? 1 : 0;
         wa.unscaled = (cfg.flags & MCMI_FLAG_UNSCALED) ? 1 : 0;
+        // Neighbourhood slot tables (walk.cu, L = 2): their per-row set-up costs
+        // about as much as a few thousand logged deposits, so they are used only
+        // when a row logs many more deposits than its 2-hop neighbourhood holds
+        // (C2 at eps = 0.01: 10976 vs 703, -1.6%; at the defaults, 282 deposits
+        // per row, they cost C2 +60%, C3 +17%, C4 +14%).
+        wa.nb_hint = (deposits >= 4096 && deposits / 12 >= reach) ? 1 : 0;
         wa.gscratch = nullptr;
         int64_t max_warps = 0;
         if (t.global) {

@@ -130,6 +130,7 @@ struct WalkArgs {
     long long warp_bytes;   // launch_walk: shared/global bytes per warp
     int deg_stats;          // count sum deg(s) (MCMI_FLAG_DEG_STATS)
     int unscaled;           // MCMI_FLAG_UNSCALED: rows of (I - A)^-1 (estimate_row), no scale / prune
+    int nb_hint;            // L = 2: neighbourhood slot tables pay off (deposits per row >> 2-hop size)
     unsigned char* gscratch;  // global-tier per-warp accumulator + log (nullptr for smem tiers)
     // outputs, indexed by local row (row - row_begin)
     int* stage_col;

@@ -420,7 +420,7 @@ __device__ int sort_by_column(int* keys, double* vals, int s) {
 
 constexpr int kRankTopkMax = 256;  // above this row length retain_top_k uses radix_topk
 
-// Neighbourhood slot tables (NB variant, L = 2 with the 256-slot tier): at row
+// Neighbourhood slot tables (NB variant, L = 2 with the 32/64/256-slot tiers): at row
 // start the warp inserts r's columns and its neighbours' columns into the hash
 // once and keeps T1[i] = slot of r's i-th column, T2[off[i] + j] = slot of the
 // j-th column of r's i-th neighbour.  A step then logs a slot instead of a
@@ -434,7 +434,7 @@ constexpr int kNbBytes = 32 + 2 * kNbDeg + kNbDeg + kNbT2;  // mask[8] u32, off[
 
 template <int MODE, int MINB, bool GL, bool DEG, int LF = 0, int CAPC = 0, bool NB = false>
 __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
-    static_assert(!NB || (LF == 2 && CAPC == 256 && !GL), "NB: L = 2 kernel, 256-slot shared tier");
+    static_assert(!NB || (LF == 2 && CAPC >= 32 && CAPC <= 256 && !GL), "NB: L = 2 kernel, shared tiers");
     // LF > 0: a launch with max_len == log_stride == LF and 32-lane batches:
     // the step loop (unrolled, no length or log-capacity tests) and the fold's
     // position arithmetic are compile-time.
@@ -857,7 +857,8 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                         if (slot < 0) fail = true;
                     }
                 }
-                slot = __shfl_sync(FULL_MASK, slot, leader);
+                if (NB && nb) slot = ok ? c : 0;  // the logged key is the slot
+                else slot = __shfl_sync(FULL_MASK, slot, leader);
                 const double w = ok ? sm.log_w[q] : 0.0;
                 double v = w;
                 if (ok && rank == 0 && slot >= 0) v = sm.vals[slot] + w;
@@ -1070,11 +1071,13 @@ int walk_minb() {
     return v;
 }
 
-// MCMI_WALK_NB=0 (env, tuning and tests) disables the neighbourhood slot
-// tables of the L = 2 / 256-slot kernel.
-bool walk_nb() {
+// Neighbourhood slot tables for the L = 2 kernels: the host's cost hint
+// (WalkArgs::nb_hint), overridden by MCMI_WALK_NB=0 / 1 (tuning and tests).
+bool walk_nb(const WalkArgs& a) {
     const char* e = getenv("MCMI_WALK_NB");
-    return !(e && e[0] == '0');
+    if (e && e[0] == '0') return false;
+    if (e && e[0] == '1') return true;
+    return a.nb_hint != 0;
 }
 
 // The compile-time (walk length, capacity) variants of k_walk for MODE 0 / 1;
@@ -1084,10 +1087,15 @@ bool launch_specialised(const WalkArgs& a, int wpb, int sms, cudaStream_t s, cud
     if (a.lanes != 32 || a.log_stride != a.max_len) return false;
     switch (a.max_len) {
         case 2:
+            if (walk_nb(a) && (a.cap == 32 || a.cap == 64 || a.cap == 256)) {
+                *err = a.cap == 32   ? launch_walk_t<MODE, 6, false, false, 2, 32, true>(a, wpb, sms, 0, s)
+                       : a.cap == 64 ? launch_walk_t<MODE, 6, false, false, 2, 64, true>(a, wpb, sms, 0, s)
+                                     : launch_walk_t<MODE, 6, false, false, 2, 256, true>(a, wpb, sms, 0, s);
+                return true;
+            }
             *err = a.cap == 32    ? launch_walk_t<MODE, 6, false, false, 2, 32>(a, wpb, sms, 0, s)
                    : a.cap == 64  ? launch_walk_t<MODE, 6, false, false, 2, 64>(a, wpb, sms, 0, s)
-                   : a.cap == 256 ? (walk_nb() ? launch_walk_t<MODE, 6, false, false, 2, 256, true>(a, wpb, sms, 0, s)
-                                               : launch_walk_t<MODE, 6, false, false, 2, 256>(a, wpb, sms, 0, s))
+                   : a.cap == 256 ? launch_walk_t<MODE, 6, false, false, 2, 256>(a, wpb, sms, 0, s)
                                   : launch_walk_t<MODE, 6, false, false, 2>(a, wpb, sms, 0, s);
             return true;
         case 3:

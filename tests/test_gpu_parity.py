@@ -422,7 +422,8 @@ def test_walk_length_specialisations_match_generic(mc, oracle_mod, rng, max_len)
 @pytest.mark.parametrize("rng", [0, 1])
 @pytest.mark.parametrize("over", [{}, {"epsilon": 0.02, "delta": 0.01}, {"retain_k": 20, "master_seed": 3},
                                   {"chains_override": 77, "max_len_override": 2, "delta": 0.2}])
-def test_neighbourhood_slot_tables_match_plain_kernel(mc, oracle_mod, rng, over):
+@pytest.mark.parametrize("gen,cap", [("stencil27", 256), ("laplacian3d", 64), ("convdiff", 32)])
+def test_neighbourhood_slot_tables_match_plain_kernel(mc, oracle_mod, rng, over, gen, cap):
     """The L = 2 / 256-slot kernel with neighbourhood slot tables (default)
     equals the plain kernel (MCMI_WALK_NB=0) bit for bit, RowMeta included, and
     the oracle on sampled rows.  stencil27 interiors use the tables (deg 26,
@@ -430,10 +431,15 @@ def test_neighbourhood_slot_tables_match_plain_kernel(mc, oracle_mod, rng, over)
     after one step) cover mixed and unvisited neighbourhood columns."""
     import os
     from paper_2409_03095_b200 import generators as G
-    b = G.stencil27(14, 13, 12, seed=4)
+    b = {"stencil27": lambda: G.stencil27(14, 13, 12, seed=4), "laplacian3d": lambda: G.laplacian3d(13),
+         "convdiff": lambda: G.convection_diffusion(40)}[gen]()
     cfg = mc.McConfig(rng_mode=rng, **over)
-    nbk = mc.compute_preconditioner(b, cfg)
-    assert nbk.stats["hash_cap"] == 256 and nbk.budget_echo.max_len == 2
+    os.environ["MCMI_WALK_NB"] = "1"  # tables on regardless of the host's cost hint
+    try:
+        nbk = mc.compute_preconditioner(b, cfg)
+    finally:
+        del os.environ["MCMI_WALK_NB"]
+    assert nbk.stats["hash_cap"] == cap and nbk.budget_echo.max_len == 2
     os.environ["MCMI_WALK_NB"] = "0"
     try:
         plain = mc.compute_preconditioner(b, cfg)
