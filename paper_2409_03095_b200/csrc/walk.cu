@@ -531,33 +531,14 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                         else nb_t1[lane] = static_cast<unsigned char>(sl);
                     }
                     __syncwarp();
-                    // the 2-hop lists flattened over the warp, four positions per
-                    // lane in flight (loads first, then the probes); position p
-                    // belongs to the last neighbour i with off[i] <= p.  Equal
-                    // columns inserted concurrently resolve through the CAS.
-                    for (unsigned p0 = 0; p0 < tot; p0 += 128) {
-                        int cc[4];
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const unsigned p = p0 + 32u * u + lane;
-                            int lo = 0, hi = static_cast<int>(dr);
-                            while (hi - lo > 1) {
-                                const int mid = (lo + hi) >> 1;
-                                if (nb_off[mid] <= p) lo = mid;
-                                else hi = mid;
-                            }
-                            const unsigned bi = __shfl_sync(FULL_MASK, ba, lo);
-                            const unsigned oi = __shfl_sync(FULL_MASK, offa, lo);
-                            cc[u] = p < tot ? tcol[bi + (p - oi)] : 0;
-                        }
-#pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const unsigned p = p0 + 32u * u + lane;
-                            if (p < tot) {
-                                const int sl = hash_slot<false>(sm.keys, cap_mask, shift, cc[u], nn);
-                                if (sl < 0) bad = true;
-                                else nb_t2[p] = static_cast<unsigned char>(sl);
-                            }
+                    for (unsigned i = 0; i < dr; ++i) {
+                        const unsigned di = __shfl_sync(FULL_MASK, da, i);
+                        const unsigned bi = __shfl_sync(FULL_MASK, ba, i);
+                        const unsigned oi = __shfl_sync(FULL_MASK, offa, i);
+                        for (unsigned j = lane; j < di; j += 32) {
+                            const int sl = hash_slot<false>(sm.keys, cap_mask, shift, tcol[bi + j], nn);
+                            if (sl < 0) bad = true;
+                            else nb_t2[oi + j] = static_cast<unsigned char>(sl);
                         }
                         __syncwarp();
                     }
