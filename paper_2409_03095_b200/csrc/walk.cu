@@ -381,7 +381,8 @@ __device__ __forceinline__ void warp_rank_sort(int* keys, double* vals, int s) {
 }
 
 // Sorts (keys, vals)[0, s) by column: rank sorts for s <= 128 (register rank
-// sort for s <= 32), bitonic otherwise (pads [s, P) with INT_MAX); returns the
+// sort for s <= 32; 2, 3 or 4 entries per lane up to 64 / 96 / 128), bitonic
+// otherwise (pads [s, P) with INT_MAX); returns the
 // padded length touched.
 __device__ int sort_by_column(int* keys, double* vals, int s) {
     const int lane = static_cast<int>(threadIdx.x & 31);
@@ -401,6 +402,10 @@ __device__ int sort_by_column(int* keys, double* vals, int s) {
     }
     if (s <= 64) {
         warp_rank_sort<2>(keys, vals, s);
+        return s;
+    }
+    if (s <= 96) {
+        warp_rank_sort<3>(keys, vals, s);
         return s;
     }
     if (s <= 128) {
