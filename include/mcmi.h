@@ -127,7 +127,11 @@ typedef struct mcmi_stats {
 
 typedef struct mcmi_result mcmi_result;
 
-/* compute_preconditioner: host CSR in, host result out (H2D/D2H inside). */
+/* compute_preconditioner: host CSR in, host result out.  B may be pageable
+ * (staged through pinned bounce buffers) or page-locked.  The result is
+ * host-resident in library-owned page-locked arrays (pooled across builds),
+ * filled by a streamed build: each row chunk's device->host copy overlaps the
+ * next chunk's walks.  No output size is needed in advance. */
 int mcmi_build(const mcmi_csr_view* b, const mcmi_config* cfg, mcmi_result** out, char* err,
                size_t errlen);
 /* Same, restricted to rows [row_begin, row_end) of M (a row shard: the
@@ -176,6 +180,37 @@ int mcmi_split_copy(const mcmi_split_system* s, int64_t* b_hat_row_ptr, int64_t*
                     double* s_diag);
 void mcmi_split_free(mcmi_split_system* s);
 
+/* mcspai::estimate_row (mc_engine.hpp:63-65, mc_engine.cpp:80-122) on a
+ * caller-built SplitSystem, for rows [row_begin, row_end) at once: a = split.a
+ * (host CSR), p_values = split.p's values on A's pattern (nnz(A) doubles),
+ * budget (n_chains >= 1, max_len), delta, and row r's stream RngStream(seed, r)
+ * (rng_mode MCMI_RNG_REFERENCE) or the keyed stream.  Row r of the result is
+ * exactly estimate_row's SparseRow: columns sorted, values unscaled, nothing
+ * pruned or retained (b1_diag is not needed).  The tables are built from A and
+ * P on `device` per call (O(nnz) there; estimate_row itself allocates O(n)
+ * per call, mc_engine.cpp:120).  Result: as mcmi_build_rows (RowMeta
+ * chains_used = chains_run). */
+int mcmi_estimate_rows(const mcmi_csr_view* a, const double* p_values, int64_t row_begin, int64_t row_end,
+                       int64_t n_chains, int64_t max_len, double delta, uint64_t seed, int32_t rng_mode, int device,
+                       mcmi_result** out, char* err, size_t errlen);
+
+/* mcspai::retain_top_k (mc_engine.hpp:70, mc_engine.cpp:124-145) on every row
+ * of a host CSR at once (each row one SparseRow): row r keeps the k entries
+ * ranked first by (column == diag_cols[r] first, |value| descending, column
+ * ascending), in their original order; rows with <= k entries, and every row
+ * when k <= 0, are unchanged.  diag_cols NULL means diag_cols[r] = r.
+ * out_row_ptr[n+1]; out_col_idx / out_values hold nnz(rows) entries; *out_nnz
+ * = entries kept.  (The build applies the same rule inside the walk kernel.) */
+int mcmi_retain_top_k(const mcmi_csr_view* rows, int64_t k, const int64_t* diag_cols, int device,
+                      int64_t* out_row_ptr, int64_t* out_col_idx, double* out_values, int64_t* out_nnz, char* err,
+                      size_t errlen);
+/* mcspai::scale_columns (mc_engine.hpp:74, mc_engine.cpp:147-149) on every
+ * entry of a host CSR: out_values[i] = values[i] / b1_diag[col_idx[i]].
+ * MCMI_ERANGE if a column is outside [0, b1_len) (the reference indexes
+ * without a check). */
+int mcmi_scale_columns(const mcmi_csr_view* rows, const double* b1_diag, int64_t b1_len, int device,
+                       double* out_values, char* err, size_t errlen);
+
 /* mcspai::transition_probabilities (split.hpp:39) of any CSR A on `device`:
  * p_ij = |a_ij| / sequential row sum; rows summing to 0 become empty.
  * p_row_ptr[n+1]; p_col_idx / p_values hold nnz(A) entries; *p_nnz = entries
@@ -196,13 +231,32 @@ int mcmi_drop_small_entries(const mcmi_csr_view* m, double p, int32_t drop_mode,
  * reaches total*g/parts.  Used by host builds with n_gpus > 1 and by the
  * one-process-per-GPU driver (distributed.partition_rows).  Host only. */
 int mcmi_partition_rows(const int64_t* row_ptr, int64_t row_begin, int64_t row_end, int parts, int64_t* edges);
+/* The same build of rows [row_begin, row_end) started on a library thread, for
+ * callers that size their own output while the walks run (the C++ drop-in,
+ * include/mcmi/mcspai_compat.hpp): B's arrays must stay valid until
+ * mcmi_job_finish.  mcmi_job_estimate blocks until the first row chunk (10% of
+ * the rows) is built and returns an upper-biased extrapolation of nnz(M)
+ * (x1.06 + 1024; exact when the build has a single chunk), or -1 with the
+ * build's error status if it failed first.  mcmi_job_finish waits for the
+ * build and returns its result (to be freed with mcmi_result_free), or the
+ * build's error; it frees the job. */
+typedef struct mcmi_job mcmi_job;
+int mcmi_build_start(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_begin, int64_t row_end,
+                     mcmi_job** job, char* err, size_t errlen);
+int mcmi_job_estimate(mcmi_job* job, int64_t* nnz_estimate);
+int mcmi_job_finish(mcmi_job* job, mcmi_result** out, char* err, size_t errlen);
+
 int mcmi_result_sizes(const mcmi_result* r, int64_t* n, int64_t* nnz);
 /* Any pointer may be NULL.  row_ptr[n+1], col_idx[nnz], values[nnz],
  * chains_used[n] / entries_before[n] = RowMeta (mc_engine.hpp:33-36),
- * n_chains / max_len = budget_echo. */
+ * n_chains / max_len = budget_echo.  A multi-threaded host copy. */
 int mcmi_result_copy(const mcmi_result* r, int64_t* row_ptr, int64_t* col_idx, double* values,
                      int64_t* chains_used, int64_t* entries_before, int64_t* n_chains,
                      int64_t* max_len);
+/* Borrowed pointers to the result's host arrays (valid until mcmi_result_free;
+ * col_idx / values are NULL when nnz == 0): zero-copy access for bindings. */
+int mcmi_result_view(const mcmi_result* r, const int64_t** row_ptr, const int64_t** col_idx, const double** values,
+                     const int64_t** chains_used, const int64_t** entries_before);
 int mcmi_result_stats(const mcmi_result* r, mcmi_stats* stats);
 void mcmi_result_free(mcmi_result* r);
 

@@ -60,6 +60,8 @@ def lib():
         L = C.CDLL(LIB_PATH)
         L.ref_build.argtypes = [C.c_int64, _i64p, _i64p, _f64p, C.POINTER(RefConfig),
                                 C.c_int, C.c_int, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+        L.ref_build_timed.argtypes = [C.c_int64, _i64p, _i64p, _f64p, C.POINTER(RefConfig), C.c_int, C.c_int,
+                                      C.POINTER(C.c_void_p), C.POINTER(C.c_double), C.c_char_p, C.c_size_t]
         L.ref_result_sizes.argtypes = [C.c_void_p, _i64p, _i64p]
         L.ref_result_copy.argtypes = [C.c_void_p, _i64p, _i64p, _f64p, _i64p, _i64p, _i64p, _i64p]
         L.ref_result_write_mm.argtypes = [C.c_void_p, C.c_char_p, C.c_char_p, C.c_size_t]
@@ -87,6 +89,8 @@ def lib():
         L.ref_split_matrix.restype = C.c_void_p
         L.ref_split_diag.argtypes = [C.c_void_p, _f64p, _f64p, _f64p]
         L.ref_split_free.argtypes = [C.c_void_p]
+        L.ref_split_from_ap.argtypes = [C.c_int64, _i64p, _i64p, _f64p, _f64p]
+        L.ref_split_from_ap.restype = C.c_void_p
         L.ref_budget.argtypes = [C.POINTER(RefConfig), C.c_double, _i64p, _i64p, C.c_char_p, C.c_size_t]
         L.ref_estimate_row.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_double,
                                        C.c_uint64, _i64p, _f64p, C.c_int64]
@@ -165,6 +169,7 @@ class RefResult:
     entries_before: np.ndarray
     n_chains: int
     max_len: int
+    build_s: float = 0.0  #: wall time of the reference call alone (ref_build_timed)
 
 
 def _check(code, err):
@@ -173,15 +178,23 @@ def _check(code, err):
 
 
 def compute_preconditioner(b: Csr, n_threads: int = 0, serial: bool = False,
-                           mm_path: str | None = None, **cfg) -> RefResult:
+                           mm_path: str | None = None, copy: bool = True, **cfg) -> RefResult:
+    """The reference's compute_preconditioner(_serial) on b.  ``build_s`` is
+    the wall time of that call alone; copy=False skips copying M out (timing
+    runs)."""
     L = lib()
     c = make_config(**cfg)
     rp, ci, v = b.args()
     h = C.c_void_p()
     err = C.create_string_buffer(512)
-    code = L.ref_build(b.n, _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p), C.byref(c),
-                       n_threads, int(serial), C.byref(h), err, 512)
+    secs = C.c_double(0.0)
+    code = L.ref_build_timed(b.n, _p(rp, _i64p), _p(ci, _i64p), _p(v, _f64p), C.byref(c),
+                             n_threads, int(serial), C.byref(h), C.byref(secs), err, 512)
     _check(code, err)
+    if not copy:
+        L.ref_result_free(h)
+        return RefResult(Csr(b.n, np.zeros(1, np.int64), np.zeros(0, np.int64), np.zeros(0)),
+                         np.zeros(0, np.int64), np.zeros(0, np.int64), 0, 0, secs.value)
     try:
         n, nnz = C.c_int64(), C.c_int64()
         L.ref_result_sizes(h, C.byref(n), C.byref(nnz))
@@ -198,7 +211,7 @@ def compute_preconditioner(b: Csr, n_threads: int = 0, serial: bool = False,
     finally:
         L.ref_result_free(h)
     return RefResult(Csr(n.value, orp, oci[: nnz.value], ov[: nnz.value]),
-                     cu[: n.value], eb[: n.value], nc.value, ml.value)
+                     cu[: n.value], eb[: n.value], nc.value, ml.value, secs.value)
 
 
 # generator kinds (ref_shim.cpp ref_gen)
@@ -420,3 +433,14 @@ def solve(b: Csr, m: Csr | None, method: str = "gmres", rel_tol: float = 1e-6, m
                        _p(mv, _f64p), 0 if method == "gmres" else 1, rel_tol, max_iters, restart,
                        C.byref(it), C.byref(conv), C.byref(res), err, 512), err)
     return it.value, bool(conv.value), res.value
+
+
+def split_from_ap(n, row_ptr, col_idx, a_values, p_values):
+    """A hand-built SplitSystem handle (split.a, split.p on A's pattern); free with free_split."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    ci = np.ascontiguousarray(col_idx if len(col_idx) else np.zeros(1, np.int64), np.int64)
+    av = np.ascontiguousarray(a_values if len(a_values) else np.zeros(1), np.float64)
+    pv = np.ascontiguousarray(p_values if len(p_values) else np.zeros(1), np.float64)
+    h = lib().ref_split_from_ap(n, _p(rp, _i64p), _p(ci, _i64p), _p(av, _f64p), _p(pv, _f64p))
+    a = Csr(n, rp, ci[: rp[-1]], av[: rp[-1]])
+    return RefSplit(a, a, Csr(n, rp, ci[: rp[-1]], pv[: rp[-1]]), np.ones(n), np.zeros(n), 0.5, handle=h)

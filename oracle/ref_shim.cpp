@@ -21,6 +21,7 @@
 //   ref_solve          -> mcspai::solve (gmres / bicgstab), rhs = B*1  (solvers.hpp:35-46)
 // Exceptions are mapped to status codes: 1 invalid_argument, 2 SplitError,
 // 3 out_of_range, 4 other.
+#include <chrono>
 #include <cstdint>
 #include <cstring>
 #include <sstream>
@@ -135,20 +136,32 @@ int ref_max_threads() {
 }
 
 // ---- compute_preconditioner ------------------------------------------------
-int ref_build(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
-              const ref_config* c, int n_threads, int serial, void** out,
-              char* err, size_t errlen) {
+// seconds (may be NULL) receives the wall time of the reference call alone:
+// the CsrMatrix is built before the clock starts, as a reference caller holds
+// one already (bench.py --impl reference times exactly this).
+int ref_build_timed(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+                    const ref_config* c, int n_threads, int serial, void** out,
+                    double* seconds, char* err, size_t errlen) {
     *out = nullptr;
     return guarded(
         [&] {
             const CsrMatrix b = to_csr(n, rp, ci, v);
             const McConfig cfg = to_cfg(c);
+            const auto t0 = std::chrono::steady_clock::now();
             auto res = std::make_unique<ApproxInverse>(
                 serial ? compute_preconditioner_serial(b, cfg)
                        : compute_preconditioner(b, cfg, n_threads));
+            const auto t1 = std::chrono::steady_clock::now();
+            if (seconds) *seconds = std::chrono::duration<double>(t1 - t0).count();
             *out = res.release();
         },
         err, errlen);
+}
+
+int ref_build(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
+              const ref_config* c, int n_threads, int serial, void** out,
+              char* err, size_t errlen) {
+    return ref_build_timed(n, rp, ci, v, c, n_threads, serial, out, nullptr, err, errlen);
 }
 
 void ref_result_sizes(const void* h, int64_t* n, int64_t* nnz) {
@@ -309,6 +322,18 @@ int ref_split(int64_t n, const int64_t* rp, const int64_t* ci, const double* v,
                 mode == 0 ? AugmentationMode::plain : AugmentationMode::sign_aware));
         },
         err, errlen);
+}
+
+// A caller-built SplitSystem (the reference's own tests build one by hand,
+// test_mc_engine.cpp:112-127): a = (rp, ci, av), p = A's pattern with pv.
+void* ref_split_from_ap(int64_t n, const int64_t* rp, const int64_t* ci, const double* av, const double* pv) {
+    auto* s = new SplitSystem();
+    s->a = to_csr(n, rp, ci, av);
+    s->p = to_csr(n, rp, ci, pv);
+    s->b1_diag.assign(static_cast<size_t>(n), 1.0);
+    s->s_diag.assign(static_cast<size_t>(n), 0.0);
+    s->a_norm = 0.5;
+    return s;
 }
 
 // which: 0 b_hat, 1 a, 2 p

@@ -25,6 +25,8 @@ EXPORTS = [
     "mcmi_host_csr_get", "mcmi_host_csr_free", "mcmi_mm_format", "mcmi_mm_write_file", "mcmi_recover_inverse",
     "mcmi_recover_inverse_device", "mcmi_scatter_shard", "mcmi_derive_chain_budget", "mcmi_augment_and_split",
     "mcmi_split_sizes", "mcmi_split_copy", "mcmi_split_free", "mcmi_transition_probabilities", "mcmi_drop_small_entries",
+    "mcmi_build_start", "mcmi_job_estimate", "mcmi_job_finish", "mcmi_result_view", "mcmi_estimate_rows",
+    "mcmi_retain_top_k", "mcmi_scale_columns",
 ]
 
 
@@ -141,6 +143,18 @@ def load(path: str | None = None):
                                                 C.c_char_p, C.c_size_t]
     L.mcmi_result_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                    _i64p, _i64p]
+    L.mcmi_result_view.argtypes = [C.c_void_p] + [C.POINTER(C.c_void_p)] * 5
+    L.mcmi_build_start.argtypes = [C.POINTER(mcmi_csr_view), C.POINTER(mcmi_config), C.c_int64, C.c_int64,
+                                   C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+    L.mcmi_job_estimate.argtypes = [C.c_void_p, _i64p]
+    L.mcmi_retain_top_k.argtypes = [C.POINTER(mcmi_csr_view), C.c_int64, C.c_void_p, C.c_int, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, _i64p, C.c_char_p, C.c_size_t]
+    L.mcmi_scale_columns.argtypes = [C.POINTER(mcmi_csr_view), C.c_void_p, C.c_int64, C.c_int, C.c_void_p,
+                                     C.c_char_p, C.c_size_t]
+    L.mcmi_estimate_rows.argtypes = [C.POINTER(mcmi_csr_view), C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                                     C.c_int64, C.c_double, C.c_uint64, C.c_int32, C.c_int, C.POINTER(C.c_void_p),
+                                     C.c_char_p, C.c_size_t]
+    L.mcmi_job_finish.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
     L.mcmi_result_stats.argtypes = [C.c_void_p, C.POINTER(mcmi_stats)]
     L.mcmi_result_free.argtypes = [C.c_void_p]
     L.mcmi_result_free.restype = None

@@ -13,6 +13,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <condition_variable>
+#include <functional>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -20,6 +22,7 @@
 
 #include "mcmi.h"
 #include "kernels.cuh"
+#include "hostio.h"
 
 using namespace mcmi;
 
@@ -281,20 +284,41 @@ Tier make_global_tier(int64_t bound, int64_t max_len, int64_t min_cap = 8192) {
     return t;
 }
 
-// The full build of rows [row_begin, row_end) from device CSR `b`.
-// Caller-owned host arrays for the streamed build (mcmi_build_into).
+// Host destination of a streamed build (mcmi_build_into: caller-owned arrays;
+// mcmi_build / mcmi_job_*: library-owned pinned buffers that grow on demand).
 struct HostSink {
-    int64_t* row_ptr;
-    int64_t* col_idx;
-    double* values;
-    int64_t capacity;
-    int64_t* chains_used;
-    int64_t* entries_before;
+    int64_t* row_ptr = nullptr;  // [rows + 1]
+    int64_t* col_idx = nullptr;
+    double* values = nullptr;
+    int64_t capacity = 0;  // entries col_idx / values hold
+    int64_t* chains_used = nullptr;
+    int64_t* entries_before = nullptr;
+    // Library-owned output: called (copy stream drained) when entries [0, need)
+    // must fit; may re-point col_idx / values keeping entries [0, have).
+    // `estimate` extrapolates the final entry count from the rows built so far.
+    std::function<Status(HostSink&, int64_t need, int64_t estimate, int64_t have)> grow;
+    // After each row chunk's entry count is known: (rows done, entries so far, rows).
+    std::function<void(int64_t, int64_t, int64_t)> progress;
+    double first_chunk = 0.0;  // > 0: fraction of the rows in the first chunk (an early estimate)
+};
+
+// Device staging budget of one row chunk (stage_col + stage_val); rows are
+// walked in chunks when rows x slot stride would exceed it.
+int64_t staging_budget_bytes() {
+    const char* v = getenv("MCMI_STAGE_BUDGET_MB");  // tests / tuning
+    return v && *v ? std::max<int64_t>(1, atoll(v)) << 20 : int64_t{8} << 30;
+}
+
+// estimate_row on a caller-built SplitSystem (mcmi_estimate_rows): `b` is then
+// split.a, the tables come from A and P's values, the budget is the caller's.
+struct ApSource {
+    const double* p_values;  // device, on A's pattern
+    int64_t n_chains, max_len;
 };
 
 Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& cfg,
                     int64_t row_begin, int64_t row_end, cudaStream_t s, mcmi_device_csr* out,
-                    mcmi_stats* stats, const HostSink* sink = nullptr) {
+                    mcmi_stats* stats, HostSink* sink = nullptr, const ApSource* ap = nullptr) {
     const int64_t n = b.n;
     mcmi_stats st{};
     if (n < 0) return fail(MCMI_EINVAL, "negative dimension");
@@ -373,16 +397,22 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     ta.ent = e->ent.as<double2>();
     ta.col = e->colA.as<int>();
     ta.b1_diag = e->b1.as<double>();
-    const bool drop_active = cfg.drop_fraction != 0.0 && n > 0;
+    const bool drop_active = !ap && cfg.drop_fraction != 0.0 && n > 0;
     const int64_t scan_launches_n = (n > 0 ? 3 : 1);
-    if (drop_active && cfg.drop_mode == MCMI_DROP_COUNT_QUANTILE) {
+    if (ap) {
+        if (nnz >= (int64_t{1} << 32)) return fail(MCMI_EINVAL, "A has 2^32 or more entries");
+        const ApTableArgs aa{n,          b.row_ptr,  b.col_idx, b.values, ap->p_values, e->red.as<Reductions>(),
+                             ta.rec,     ta.ent,     ta.col,    ta.b1_diag};
+        MCMI_TRY(launch_ap_tables(aa, s), "tables from A and P");
+        st.launches += n > 0 ? 1 : 0;
+    } else if (drop_active && cfg.drop_mode == MCMI_DROP_COUNT_QUANTILE) {
         MCMI_TRY(e->keep.ensure(z1), "alloc keep");
         MCMI_TRY(e->cq_tmp.ensure(count_quantile_scratch_bytes(z1)), "alloc cq");
         ta.keep = e->keep.as<unsigned char>();
         MCMI_TRY(launch_count_quantile(ta, nnz, 0, e->cq_tmp.p, e->cq_tmp.cap, s), "count-quantile drop");
         st.launches += 2 + 2 * 8 + 1 + (nnz > 0 ? 3 : 1) + 1;
     }
-    if (n > 0) {
+    if (n > 0 && !ap) {
         MCMI_TRY(launch_table_build(ta, nnz, drop_active, s), "table build");
         MCMI_TRY(scan_u32_exclusive(ta.a_cnt, ta.a_off, n, e->scan_tmp.p, s), "scan a_cnt");
         MCMI_TRY(launch_table_fill(ta, s), "table fill");
@@ -395,17 +425,23 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     const Reductions red = *e->h_red;
     if (red.bad_col_row != LLONG_MAX)
         return fail(MCMI_ERANGE, "column index out of range in row " + std::to_string(red.bad_col_row));
-    if (red.degenerate_row != LLONG_MAX)  // split.cpp:67-69
-        return fail(MCMI_ESPLIT, "degenerate diagonal after augmentation at row " +
-                                     std::to_string(red.degenerate_row));
-    double a_norm;
-    std::memcpy(&a_norm, &red.anorm_bits, sizeof(double));
-    if (!(a_norm < 1.0))  // split.cpp:94-96
-        return fail(MCMI_ESPLIT, "diagonal dominance failure: ||A||inf = " + std::to_string(a_norm));
-    if (red.a_nnz >= (1ull << 32)) return fail(MCMI_EINVAL, "A has 2^32 or more entries");
+    double a_norm = 0.0;
     int64_t N = 1, L = 1;
-    Status bs = chain_budget(cfg, a_norm, &N, &L);
-    if (bs.code) return bs;
+    if (ap) {
+        N = ap->n_chains;
+        L = ap->max_len;
+        if (N < 1) return fail(MCMI_EINVAL, "n_chains must be positive");
+    } else {
+        if (red.degenerate_row != LLONG_MAX)  // split.cpp:67-69
+            return fail(MCMI_ESPLIT, "degenerate diagonal after augmentation at row " +
+                                         std::to_string(red.degenerate_row));
+        std::memcpy(&a_norm, &red.anorm_bits, sizeof(double));
+        if (!(a_norm < 1.0))  // split.cpp:94-96
+            return fail(MCMI_ESPLIT, "diagonal dominance failure: ||A||inf = " + std::to_string(a_norm));
+        if (red.a_nnz >= (1ull << 32)) return fail(MCMI_EINVAL, "A has 2^32 or more entries");
+        Status bs = chain_budget(cfg, a_norm, &N, &L);
+        if (bs.code) return bs;
+    }
     if (N > INT_MAX) return fail(MCMI_EINVAL, "chain budget exceeds 2^31-1 chains per row");
     // walk lengths: the deposit log holds min(L, 65536) steps per chain; a walk
     // that would outgrow its tier's log overflows the row to the next tier, and
@@ -479,7 +515,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         wa.work_offset = offset;
         wa.n_work = work;
         wa.n_chains = N;
-        wa.max_len = std::min<int64_t>(L, INT_MAX);  // walks beyond the log capacity overflow anyway
+        wa.max_len = std::clamp<int64_t>(L, 0, INT_MAX);  // walks beyond the log capacity overflow anyway
         wa.delta = cfg.delta;
         wa.seed = cfg.master_seed;
         wa.retain_k = cfg.retain_k;
@@ -619,82 +655,116 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         return ok();
     };
 
-    int64_t out_nnz = 0;
+    // ---- rows in chunks, each walked, scanned and compacted in row order
+    // (mc_engine.cpp:207-225).  Device output (no sink): one chunk unless
+    // rows x slot stride exceeds the staging budget; entries are appended to the
+    // engine's output buffers.  Host sink: chunk sizes fall geometrically (few
+    // chunk boundaries, each costs the walk kernel's tail, and a small last
+    // chunk, whose copy is the exposed one); chunk c's device->host copy (copy
+    // stream) overlaps chunk c+1's walk, through double-buffered device slabs.
+    // MCMI_STREAM_CHUNKS / MCMI_STREAM_RATIO: tuning overrides.
+    const int64_t entry_bytes = static_cast<int64_t>(sizeof(int) + sizeof(double));
+    const int64_t budget_rows =
+        std::max<int64_t>(pilot_rows + 1, staging_budget_bytes() / (stride_of(tiers[t0]) * entry_bytes));
+    std::vector<int64_t> bnd{0};
     if (!sink) {
-        // ---- one pass: all rows, then assembly into the engine's buffers
-        Status ws = walk_rows(pilot_rows, rows);
-        if (ws.code) return ws;
-        MCMI_TRY(cudaEventRecord(e->ev[2], s), "cudaEventRecord");
-        // ---- assembly (mc_engine.cpp:207-225)
-        MCMI_TRY(e->out_rp.ensure((rows + 1) * sizeof(int64_t)), "alloc row_ptr");
-        MCMI_TRY(scan_rows_exclusive(e->row_cnt.as<int>(), e->out_rp.as<int64_t>(), rows, e->scan_tmp.p, s),
-                 "scan rows");
-        MCMI_TRY(cudaMemcpyAsync(e->h_i64, e->out_rp.as<int64_t>() + rows, sizeof(int64_t),
-                                 cudaMemcpyDeviceToHost, s),
-                 "read nnz");
-        MCMI_TRY(cudaStreamSynchronize(s), "scan rows");
-        out_nnz = e->h_i64[0];
-        MCMI_TRY(e->out_col.ensure(std::max<int64_t>(out_nnz, 1) * sizeof(int64_t)), "alloc col");
-        MCMI_TRY(e->out_val.ensure(std::max<int64_t>(out_nnz, 1) * sizeof(double)), "alloc val");
-        MCMI_TRY(launch_compact(e->stage_col.as<int>(), e->stage_val.as<double>(), e->row_src.as<int64_t>(),
-                                e->row_cnt.as<int>(), e->out_rp.as<int64_t>(), rows, e->out_col.as<int64_t>(),
-                                e->out_val.as<double>(), s),
-                 "compact");
-        st.launches += (rows > 0 ? 3 : 1) + (rows > 0 ? 1 : 0);
+        const int64_t nch = std::max<int64_t>(1, (rows + budget_rows - 1) / budget_rows);
+        for (int64_t c = 1; c <= nch; ++c) bnd.push_back(std::max(bnd.back(), rows * c / nch));
     } else {
-        // ---- streamed: row chunks; chunk c's device->host copy (copy stream)
-        // overlaps chunk c+1's walk (compute stream).  Double-buffered slabs.
-        // Chunk sizes fall geometrically: few chunk boundaries (each costs the
-        // walk kernel's tail) and a small last chunk (its copy is the exposed
-        // one).  MCMI_STREAM_CHUNKS / MCMI_STREAM_RATIO: tuning overrides.
         int64_t nchunk = std::max<int64_t>(1, std::min<int64_t>(8, rows / 65536));
         double ratio = 0.65;
         if (const char* v = getenv("MCMI_STREAM_CHUNKS")) nchunk = std::max<int64_t>(1, std::min<int64_t>(64, atoll(v)));
         if (const char* v = getenv("MCMI_STREAM_RATIO")) ratio = std::max(0.05, std::min(1.0, atof(v)));
         nchunk = std::min<int64_t>(nchunk, std::max<int64_t>(rows, 1));
-        std::vector<int64_t> bound(nchunk + 1, 0);
-        {
-            double wsum = 0.0, w = 1.0;
-            for (int64_t c = 0; c < nchunk; ++c, w *= ratio) wsum += w;
-            double acc = 0.0;
-            w = 1.0;
-            for (int64_t c = 1; c < nchunk; ++c, w *= ratio) {
-                acc += w;
-                bound[c] = std::max(bound[c - 1] + 1, static_cast<int64_t>(static_cast<double>(rows) * acc / wsum));
-            }
-            bound[nchunk] = rows;
+        int64_t start = 0;
+        if (sink->first_chunk > 0.0 && nchunk > 1) {  // a small first chunk: an early entry-count estimate
+            start = std::max<int64_t>(1, static_cast<int64_t>(static_cast<double>(rows) * sink->first_chunk));
+            bnd.push_back(start);
+            --nchunk;
         }
+        double wsum = 0.0, w = 1.0;
+        for (int64_t c = 0; c < nchunk; ++c, w *= ratio) wsum += w;
+        double acc = 0.0;
+        w = 1.0;
+        for (int64_t c = 1; c < nchunk; ++c, w *= ratio) {
+            acc += w;
+            bnd.push_back(std::max(bnd.back() + 1,
+                                   start + static_cast<int64_t>(static_cast<double>(rows - start) * acc / wsum)));
+        }
+        bnd.push_back(rows);
+        // no chunk larger than the staging budget
+        std::vector<int64_t> split{0};
+        for (size_t c = 1; c < bnd.size(); ++c)
+            for (int64_t x = split.back(); x < bnd[c];) split.push_back(x = std::min(bnd[c], x + budget_rows));
+        bnd.swap(split);
+    }
+    if (bnd.size() > 1 && bnd[1] < pilot_rows) bnd[1] = pilot_rows;  // chunk 0 holds the pilot rows
+    for (size_t c = 1; c < bnd.size(); ++c) bnd[c] = std::min(rows, std::max(bnd[c], bnd[c - 1]));
+    const int64_t nchunk = static_cast<int64_t>(bnd.size()) - 1;
+
+    MCMI_TRY(e->out_rp.ensure((rows + 1) * sizeof(int64_t)), "alloc row_ptr");
+    if (sink) {
         MCMI_TRY(e->ensure_copy_stream(), "copy stream");
         MCMI_TRY(cudaStreamSynchronize(e->copy), "drain copies");
-        // row pointers of all chunks accumulate in out_rp; only col/val stream per chunk
-        // (small per-chunk copies into pageable memory would block the host behind
-        // the copy stream and serialise it with the walks)
-        MCMI_TRY(e->out_rp.ensure((rows + 1) * sizeof(int64_t)), "alloc row_ptr");
-        int64_t slab_cap = static_cast<int64_t>(std::min(e->col_slab[0].cap / sizeof(int64_t),
-                                                         e->val_slab[0].cap / sizeof(double)));
-        int64_t running = 0;
-        bool fits = true;
-        // MCMI_STREAM_DEBUG=1: per-chunk device timestamps of walk and copy
-        const bool dbg = getenv("MCMI_STREAM_DEBUG") != nullptr;
-        std::vector<cudaEvent_t> dev(dbg ? 4 * nchunk : 0);
-        for (auto& ev : dev) cudaEventCreate(&ev);
-        for (int64_t c = 0; c < nchunk; ++c) {
-            if (dbg) cudaEventRecord(dev[4 * c], s);
-            const int64_t lo = bound[c], hi = std::min(rows, bound[c + 1]);
-            if (lo >= hi) continue;
-            if (c > 0) pool_used = 0;  // staging reused per chunk (chunk 0 keeps the pilot rows' slots)
-            Status ws = walk_rows(c == 0 ? pilot_rows : lo, hi);
-            if (ws.code) return ws;
-            if (dbg) cudaEventRecord(dev[4 * c + 1], s);
-            const int64_t cr = hi - lo;
-            int64_t* rp_chunk = e->out_rp.as<int64_t>() + lo;  // chunk-local offsets, then global
-            // wait until chunk c-2's copies released this slab pair
-            MCMI_TRY(cudaStreamWaitEvent(s, e->copy_done[c & 1], 0), "wait copy");
-            MCMI_TRY(scan_rows_exclusive(e->row_cnt.as<int>() + lo, rp_chunk, cr, e->scan_tmp.p, s), "scan rows");
-            MCMI_TRY(cudaMemcpyAsync(e->h_i64, rp_chunk + cr, sizeof(int64_t), cudaMemcpyDeviceToHost, s),
-                     "read chunk nnz");
-            MCMI_TRY(cudaStreamSynchronize(s), "scan rows");
-            const int64_t cn = e->h_i64[0];
+    }
+    // every exit (errors included) waits for the queued copies into the sink
+    struct CopyDrain {
+        cudaStream_t s;
+        ~CopyDrain() {
+            if (s) cudaStreamSynchronize(s);
+        }
+    } drain{sink ? e->copy : nullptr};
+    int64_t slab_cap = static_cast<int64_t>(std::min(e->col_slab[0].cap / sizeof(int64_t),
+                                                     e->val_slab[0].cap / sizeof(double)));
+    int64_t running = 0;
+    bool fits = true;
+    // MCMI_STREAM_DEBUG=1: per-chunk device timestamps of walk and copy
+    const bool dbg = sink && getenv("MCMI_STREAM_DEBUG") != nullptr;
+    std::vector<cudaEvent_t> dev(dbg ? 4 * nchunk : 0);
+    for (auto& ev : dev) cudaEventCreate(&ev);
+    for (int64_t c = 0; c < nchunk; ++c) {
+        const int64_t lo = bnd[c], hi = bnd[c + 1];  // empty only when rows == 0 (the scan writes row_ptr[0])
+        if (dbg) cudaEventRecord(dev[4 * c], s);
+        if (c > 0) pool_used = 0;  // staging reused per chunk (chunk 0 keeps the pilot rows' slots)
+        Status ws = walk_rows(c == 0 ? pilot_rows : lo, hi);
+        if (ws.code) return ws;
+        if (c + 1 == nchunk) MCMI_TRY(cudaEventRecord(e->ev[2], s), "cudaEventRecord");
+        if (dbg) cudaEventRecord(dev[4 * c + 1], s);
+        const int64_t cr = hi - lo;
+        int64_t* rp_chunk = e->out_rp.as<int64_t>() + lo;  // chunk-local offsets, then global
+        // (host sink) wait until chunk c-2's copies released this slab pair
+        if (sink) MCMI_TRY(cudaStreamWaitEvent(s, e->copy_done[c & 1], 0), "wait copy");
+        MCMI_TRY(scan_rows_exclusive(e->row_cnt.as<int>() + lo, rp_chunk, cr, e->scan_tmp.p, s), "scan rows");
+        MCMI_TRY(cudaMemcpyAsync(e->h_i64, rp_chunk + cr, sizeof(int64_t), cudaMemcpyDeviceToHost, s),
+                 "read chunk nnz");
+        MCMI_TRY(cudaStreamSynchronize(s), "scan rows");
+        const int64_t cn = e->h_i64[0];
+        st.launches += (cr > 0 ? 3 : 1);
+        if (!sink) {
+            const int64_t need = std::max<int64_t>(running + cn, 1);
+            MCMI_TRY(running ? e->out_col.grow_preserve(need * sizeof(int64_t), running * sizeof(int64_t), s)
+                             : e->out_col.ensure(need * sizeof(int64_t)),
+                     "alloc col");
+            MCMI_TRY(running ? e->out_val.grow_preserve(need * sizeof(double), running * sizeof(double), s)
+                             : e->out_val.ensure(need * sizeof(double)),
+                     "alloc val");
+            MCMI_TRY(launch_compact(e->stage_col.as<int>(), e->stage_val.as<double>(), e->row_src.as<int64_t>() + lo,
+                                    e->row_cnt.as<int>() + lo, rp_chunk, cr, e->out_col.as<int64_t>() + running,
+                                    e->out_val.as<double>() + running, s),
+                     "compact");
+            st.launches += (cr > 0 ? 1 : 0);
+            if (running) {
+                MCMI_TRY(launch_add_offset(rp_chunk, running, cr, s), "row_ptr offset");
+                st.launches += 1;
+            }
+        } else {
+            if (fits && running + cn > sink->capacity && sink->grow) {
+                MCMI_TRY(cudaStreamSynchronize(e->copy), "drain copies");  // nothing in flight into the old buffer
+                const double done = static_cast<double>(std::max<int64_t>(hi, 1));
+                const int64_t est = static_cast<int64_t>(static_cast<double>(running + cn) * rows / done * 1.06) + 1024;
+                Status gs = sink->grow(*sink, running + cn, std::max(est, running + cn), running);
+                if (gs.code) return gs;
+            }
             if (running + cn > sink->capacity) fits = false;
             if (fits) {
                 if (cn > slab_cap) {
@@ -722,11 +792,17 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
                 MCMI_TRY(d2h(sink->values + running, vs, cn * sizeof(double)), "D2H val");
                 MCMI_TRY(cudaEventRecord(e->copy_done[c & 1], e->copy), "cudaEventRecord");
                 if (dbg) cudaEventRecord(dev[4 * c + 3], e->copy);
-                st.launches += 5;
+                st.launches += 2;
             }
-            running += cn;
         }
-        MCMI_TRY(cudaEventRecord(e->ev[2], s), "cudaEventRecord");
+        running += cn;
+        if (sink && sink->progress) sink->progress(hi, running, rows);
+    }
+    const int64_t out_nnz = running;
+    if (!sink) {
+        MCMI_TRY(e->out_col.ensure(sizeof(int64_t)), "alloc col");  // valid pointers for empty results
+        MCMI_TRY(e->out_val.ensure(sizeof(double)), "alloc val");
+    } else {
         MCMI_TRY(cudaStreamSynchronize(e->copy), "D2H");
         if (dbg) {
             for (int64_t c = 0; c < nchunk; ++c) {
@@ -738,9 +814,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
                 fprintf(stderr, "chunk %lld walk %.2f-%.2f copy %.2f-%.2f ms\n", static_cast<long long>(c), w0, w1,
                         c0, c1);
             }
-            for (auto& ev : dev) cudaEventDestroy(ev);
         }
-        out_nnz = running;
         if (fits) {  // row pointers and RowMeta: one copy each, after the walks
             auto cp = [&](void* dst, const void* src, size_t bytes) -> cudaError_t {
                 return (dst && bytes) ? cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s) : cudaSuccess;
@@ -758,6 +832,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
                                          std::to_string(out_nnz));
         }
     }
+    for (auto& ev : dev) cudaEventDestroy(ev);
     st.walk_steps = static_cast<int64_t>(total_steps);
     st.walk_deg_sum = (cfg.flags & MCMI_FLAG_DEG_STATS) ? static_cast<int64_t>(total_deg) : -1;
     MCMI_TRY(cudaEventRecord(e->ev[3], s), "cudaEventRecord");
@@ -817,7 +892,8 @@ void release_engine(mcmi_engine* e) {
 // Host CSR in: stage B on the engine's stream (stream-ordered pool allocations,
 // cached across calls), build rows [row_begin, row_end), release the staging.
 Status build_from_host(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& cfg, int64_t row_begin,
-                       int64_t row_end, mcmi_device_csr* dc, mcmi_stats* stats, const HostSink* sink) {
+                       int64_t row_end, mcmi_device_csr* dc, mcmi_stats* stats, HostSink* sink,
+                       const ApSource* ap_host = nullptr) {
     const int64_t n = b.n;
     if (n < 0) return fail(MCMI_EINVAL, "negative dimension");
     if (n > 0 && !b.row_ptr) return fail(MCMI_EINVAL, "null row_ptr");
@@ -826,23 +902,29 @@ Status build_from_host(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config
     if (nnz > 0 && (!b.col_idx || !b.values)) return fail(MCMI_EINVAL, "null col_idx / values");
     MCMI_TRY(cudaSetDevice(e->device), "cudaSetDevice");
     cudaStream_t s = e->own;
-    void *d_rp = nullptr, *d_ci = nullptr, *d_v = nullptr;
+    void *d_rp = nullptr, *d_ci = nullptr, *d_v = nullptr, *d_p = nullptr;
+    if (ap_host) MCMI_TRY(cudaMallocAsync(&d_p, std::max<int64_t>(nnz, 1) * sizeof(double), s), "alloc P");
     MCMI_TRY(cudaMallocAsync(&d_rp, (n + 1) * sizeof(int64_t), s), "alloc B");
     MCMI_TRY(cudaMallocAsync(&d_ci, std::max<int64_t>(nnz, 1) * sizeof(int64_t), s), "alloc B");
     MCMI_TRY(cudaMallocAsync(&d_v, std::max<int64_t>(nnz, 1) * sizeof(double), s), "alloc B");
     Status st;
+    // pageable inputs (a reference caller's std::vector) go through pinned
+    // bounce buffers: 11 GB/s -> ~50 GB/s on the box (hostio.h)
     auto h2d = [&](void* dst, const void* src, size_t bytes) {
-        if (st.code == MCMI_OK && bytes)
-            st = cuda_status(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s), "H2D");
+        if (st.code == MCMI_OK && bytes) st = cuda_status(stage_h2d(dst, src, bytes, s), "H2D");
     };
     h2d(d_rp, b.row_ptr, (n + 1) * sizeof(int64_t));
     h2d(d_ci, b.col_idx, nnz * sizeof(int64_t));
     h2d(d_v, b.values, nnz * sizeof(double));
+    if (ap_host) h2d(d_p, ap_host->p_values, nnz * sizeof(double));
     if (st.code == MCMI_OK) {
         const mcmi_csr_view dv{n, static_cast<int64_t*>(d_rp), static_cast<int64_t*>(d_ci),
                                static_cast<double*>(d_v)};
-        st = engine_build(e, dv, cfg, row_begin, row_end, s, dc, stats, sink);
+        ApSource ap_dev{static_cast<const double*>(d_p), ap_host ? ap_host->n_chains : 0,
+                        ap_host ? ap_host->max_len : 0};
+        st = engine_build(e, dv, cfg, row_begin, row_end, s, dc, stats, sink, ap_host ? &ap_dev : nullptr);
     }
+    if (d_p) cudaFreeAsync(d_p, s);
     cudaFreeAsync(d_rp, s);
     cudaFreeAsync(d_ci, s);
     cudaFreeAsync(d_v, s);
@@ -851,9 +933,9 @@ Status build_from_host(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config
 
 }  // namespace
 
-// One device shard of a host build: the arrays are the engine's own output
-// buffers (no per-call device allocation or free); the result keeps the engine
-// checked out of the cache until mcmi_result_free.
+// One device shard of a multi-GPU host build: the arrays are the engine's own
+// output buffers (no per-call device allocation or free); the parts keep their
+// engines checked out of the cache until they are copied out and freed.
 struct ResultPart {
     mcmi_engine* engine = nullptr;
     int64_t rows = 0, nnz = 0;
@@ -864,11 +946,38 @@ struct ResultPart {
     const int64_t* eb = nullptr;
 };
 
-struct mcmi_result {
+struct DeviceParts {
     int64_t n = 0, nnz = 0;
     int64_t n_chains = 1, max_len = 1;
     mcmi_stats stats{};
     std::vector<ResultPart> parts;  // row blocks in row order (one per GPU)
+};
+
+// Host-resident result of mcmi_build* / mcmi_job_*: library-owned page-locked
+// arrays (pooled across builds, hostio.h), filled while the walks run.
+struct mcmi_result {
+    int64_t n = 0, nnz = 0;
+    int64_t n_chains = 1, max_len = 1;
+    mcmi_stats stats{};
+    PinnedBuf rp, ci, v, cu, eb;
+    ~mcmi_result() {
+        for (PinnedBuf* b : {&rp, &ci, &v, &cu, &eb}) pinned_release(*b);
+    }
+};
+
+// A host build running on a library thread (mcmi_build_start).
+struct mcmi_job {
+    mcmi_csr_view b{};
+    mcmi_config cfg{};
+    int64_t lo = 0, hi = -1;
+    std::thread th;
+    std::mutex mu;
+    std::condition_variable cv;
+    bool has_estimate = false, done = false;
+    int64_t estimate = -1;
+    int code = MCMI_OK;
+    std::string msg;
+    mcmi_result* result = nullptr;
 };
 
 namespace {
@@ -932,7 +1041,7 @@ std::vector<int64_t> partition_rows(const int64_t* rp, int64_t lo, int64_t hi, i
 // shard (each stages B on its own GPU); rows are independent
 // (mc_engine.cpp:164-178), so the row-ordered concatenation of the shards is
 // the single-GPU M.  On success the result owns the engines.
-Status build_parts(const mcmi_csr_view& b, const mcmi_config& cfg, int64_t lo, int64_t hi, mcmi_result* r) {
+Status build_parts(const mcmi_csr_view& b, const mcmi_config& cfg, int64_t lo, int64_t hi, DeviceParts* r) {
     std::vector<int> devs;
     if (Status st = shard_devices(cfg, &devs); st.code) return st;
     const int64_t n = b.n;
@@ -1012,7 +1121,7 @@ Status build_parts(const mcmi_csr_view& b, const mcmi_config& cfg, int64_t lo, i
 // Copies the parts to their global offsets in the caller's arrays (any pointer
 // may be NULL): every GPU's device->host copy is in flight at once, then the
 // shard-local row pointers are shifted by the entries of the shards before.
-int copy_parts(const mcmi_result* r, int64_t* row_ptr, int64_t* col_idx, double* values, int64_t* chains_used,
+int copy_parts(const DeviceParts* r, int64_t* row_ptr, int64_t* col_idx, double* values, int64_t* chains_used,
                int64_t* entries_before) {
     cudaError_t e = cudaSuccess;
     int64_t row_off = 0, nnz_off = 0;
@@ -1048,10 +1157,108 @@ int copy_parts(const mcmi_result* r, int64_t* row_ptr, int64_t* col_idx, double*
     return MCMI_OK;
 }
 
-void free_parts(mcmi_result* r) {
+void free_parts(DeviceParts* r) {
     for (ResultPart& p : r->parts)
         if (p.engine) release_engine(p.engine);
     r->parts.clear();
+}
+
+// The host drop-in's build of rows [lo, hi) into a host-resident result.  One
+// GPU: the streamed build (row chunks copied to pinned memory while the next
+// chunk walks); the entry arrays are sized from the first chunks' counts
+// (`on_estimate` receives that extrapolation, or the exact count) and grow if
+// later chunks need more.  Several GPUs (cfg.n_gpus): concurrent row blocks,
+// then every GPU's shard copied to its global offset.
+Status build_host(const mcmi_csr_view& b, const mcmi_config& cfg, int64_t lo, int64_t hi, mcmi_result* r,
+                  const std::function<void(int64_t)>& on_estimate, double first_chunk,
+                  const ApSource* ap_host = nullptr) {
+    std::vector<int> devs;
+    if (Status st = shard_devices(cfg, &devs); st.code) return st;
+    const int64_t n = b.n;
+    if (n < 0) return fail(MCMI_EINVAL, "negative dimension");
+    if (lo < 0) lo = 0;
+    if (hi < 0 || hi > n) hi = n;
+    if (hi < lo) hi = lo;
+    const int64_t rows = hi - lo;
+    auto need = [](PinnedBuf& buf, int64_t count) -> bool {
+        buf = pinned_acquire(static_cast<size_t>(std::max<int64_t>(count, 1)) * 8);
+        return buf.p != nullptr;
+    };
+    if (devs.size() > 1 && !ap_host) {
+        DeviceParts dp;
+        if (Status st = build_parts(b, cfg, lo, hi, &dp); st.code) return st;
+        if (on_estimate) on_estimate(dp.nnz);
+        Status st;
+        if (!need(r->rp, rows + 1) || !need(r->ci, dp.nnz) || !need(r->v, dp.nnz) || !need(r->cu, rows) ||
+            !need(r->eb, rows)) {
+            st = fail(MCMI_ENOMEM, "cudaHostAlloc of the result failed");
+        } else if (const int code = copy_parts(&dp, r->rp.as<int64_t>(), r->ci.as<int64_t>(), r->v.as<double>(),
+                                               r->cu.as<int64_t>(), r->eb.as<int64_t>());
+                   code) {
+            st = fail(code, "device->host copy failed");
+        }
+        r->n = dp.n;
+        r->nnz = dp.nnz;
+        r->n_chains = dp.n_chains;
+        r->max_len = dp.max_len;
+        r->stats = dp.stats;
+        free_parts(&dp);
+        return st;
+    }
+    mcmi_config c = cfg;
+    c.device = devs[0];
+    Status st;
+    mcmi_engine* e = acquire_engine(c.device, &st);
+    if (!e) return st;
+    if (!need(r->rp, rows + 1) || !need(r->cu, rows) || !need(r->eb, rows)) {
+        release_engine(e);
+        return fail(MCMI_ENOMEM, "cudaHostAlloc of the result failed");
+    }
+    HostSink sink;
+    sink.row_ptr = r->rp.as<int64_t>();
+    sink.chains_used = r->cu.as<int64_t>();
+    sink.entries_before = r->eb.as<int64_t>();
+    sink.first_chunk = first_chunk;
+    sink.grow = [r](HostSink& sk, int64_t need_n, int64_t est, int64_t have) -> Status {
+        PinnedBuf nci = pinned_acquire(static_cast<size_t>(est) * 8), nv = pinned_acquire(static_cast<size_t>(est) * 8);
+        if (!nci.p || !nv.p) {
+            pinned_release(nci);
+            pinned_release(nv);
+            return fail(MCMI_ENOMEM, "cudaHostAlloc of " + std::to_string(need_n) + " result entries failed");
+        }
+        if (have) {
+            parallel_copy(nci.p, sk.col_idx, static_cast<size_t>(have) * 8);
+            parallel_copy(nv.p, sk.values, static_cast<size_t>(have) * 8);
+        }
+        pinned_release(r->ci);
+        pinned_release(r->v);
+        r->ci = nci;
+        r->v = nv;
+        sk.col_idx = nci.as<int64_t>();
+        sk.values = nv.as<double>();
+        sk.capacity = static_cast<int64_t>(std::min(nci.bytes, nv.bytes) / 8);
+        return ok();
+    };
+    bool published = false;
+    sink.progress = [&](int64_t done, int64_t nnz_so_far, int64_t total) {
+        if (published || !on_estimate) return;
+        published = true;
+        on_estimate(done >= total ? nnz_so_far
+                                  : static_cast<int64_t>(static_cast<double>(nnz_so_far) * total /
+                                                         static_cast<double>(std::max<int64_t>(done, 1)) * 1.06) +
+                                        1024);
+    };
+    mcmi_device_csr dc{};
+    mcmi_stats ls{};
+    st = build_from_host(e, b, c, lo, hi, &dc, &ls, &sink, ap_host);
+    release_engine(e);
+    if (st.code) return st;
+    r->n = rows;
+    r->nnz = ls.nnz;
+    r->n_chains = ls.n_chains;
+    r->max_len = ls.max_len;
+    r->stats = ls;
+    return ok();
 }
 
 }  // namespace
@@ -1256,6 +1463,71 @@ Status drop_small_entries_dev(mcmi_engine* e, const mcmi_csr_view& m, double p, 
     return ok();
 }
 
+// retain_top_k (mc_engine.cpp:124-145) of every row of `m` (rowops.cu).
+Status retain_top_k_dev(mcmi_engine* e, const mcmi_csr_view& m, int64_t k, const int64_t* diag_cols, int64_t* o_rp,
+                        int64_t* o_ci, double* o_v, int64_t* o_nnz) {
+    MCMI_TRY(cudaSetDevice(e->device), "cudaSetDevice");
+    cudaStream_t s = e->own;
+    DevTemps t(s);
+    mcmi_csr_view dv{};
+    if (Status st = stage_csr(e, m, t, &dv); st.code) return st;
+    const int64_t n = m.n;
+    int64_t* d_diag = nullptr;
+    if (diag_cols && n > 0) {
+        d_diag = t.get<int64_t>(n);
+        MCMI_TRY(t.err, "alloc");
+        MCMI_TRY(cudaMemcpyAsync(d_diag, diag_cols, n * sizeof(int64_t), cudaMemcpyDefault, s), "H2D");
+    }
+    int* cnt = t.get<int>(n);
+    int64_t* orp = t.get<int64_t>(n + 1);
+    MCMI_TRY(t.err, "alloc");
+    MCMI_TRY(e->scan_tmp.ensure(scan_scratch_bytes(std::max<int64_t>(n, 1)) + 64), "alloc scan");
+    MCMI_TRY(launch_topk_rows(dv.row_ptr, dv.col_idx, dv.values, n, k, d_diag, 0, cnt, nullptr, nullptr, nullptr, s),
+             "top-k count");
+    MCMI_TRY(scan_rows_exclusive(cnt, orp, n, e->scan_tmp.p, s), "scan");
+    int64_t tot = 0;
+    if (n > 0) MCMI_TRY(cudaMemcpyAsync(&tot, orp + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+    MCMI_TRY(cudaStreamSynchronize(s), "scan");
+    int64_t* oci = t.get<int64_t>(tot);
+    double* ov = t.get<double>(tot);
+    MCMI_TRY(t.err, "alloc");
+    MCMI_TRY(launch_topk_rows(dv.row_ptr, dv.col_idx, dv.values, n, k, d_diag, 1, cnt, orp, oci, ov, s), "top-k");
+    if (n > 0) MCMI_TRY(cudaMemcpyAsync(o_rp, orp, (n + 1) * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+    if (tot) {
+        MCMI_TRY(cudaMemcpyAsync(o_ci, oci, tot * sizeof(int64_t), cudaMemcpyDeviceToHost, s), "D2H");
+        MCMI_TRY(cudaMemcpyAsync(o_v, ov, tot * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    }
+    MCMI_TRY(cudaStreamSynchronize(s), "D2H");
+    if (n == 0) o_rp[0] = 0;
+    *o_nnz = tot;
+    return ok();
+}
+
+// scale_columns (mc_engine.cpp:147-149) of every entry of `m` (rowops.cu).
+Status scale_columns_dev(mcmi_engine* e, const mcmi_csr_view& m, const double* b1, int64_t b1_len, double* o_v) {
+    MCMI_TRY(cudaSetDevice(e->device), "cudaSetDevice");
+    cudaStream_t s = e->own;
+    DevTemps t(s);
+    mcmi_csr_view dv{};
+    if (Status st = stage_csr(e, m, t, &dv); st.code) return st;
+    const int64_t nnz = m.n > 0 ? m.row_ptr[m.n] : 0;
+    if (nnz == 0) return ok();
+    double* d_b1 = t.get<double>(b1_len);
+    double* d_out = t.get<double>(nnz);
+    int* bad = t.get<int>(1);
+    MCMI_TRY(t.err, "alloc");
+    if (b1_len > 0) MCMI_TRY(cudaMemcpyAsync(d_b1, b1, b1_len * sizeof(double), cudaMemcpyDefault, s), "H2D");
+    MCMI_TRY(cudaMemsetAsync(bad, 0, sizeof(int), s), "memset");
+    MCMI_TRY(launch_scale_columns(dv.col_idx, dv.values, nnz, d_b1, b1_len, d_out, bad, s), "scale_columns");
+    int h_bad = 0;
+    MCMI_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(int), cudaMemcpyDeviceToHost, s), "D2H");
+    MCMI_TRY(cudaStreamSynchronize(s), "scale_columns");
+    if (h_bad) return fail(MCMI_ERANGE, "column index outside b1_diag");
+    MCMI_TRY(cudaMemcpyAsync(o_v, d_out, nnz * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    MCMI_TRY(cudaStreamSynchronize(s), "D2H");
+    return ok();
+}
+
 Status transition_probabilities_dev(mcmi_engine* e, const mcmi_csr_view& a, int64_t* p_rp, int64_t* p_ci,
                                     double* p_v, int64_t* p_nnz) {
     MCMI_TRY(cudaSetDevice(e->device), "cudaSetDevice");
@@ -1344,16 +1616,111 @@ int mcmi_build(const mcmi_csr_view* b, const mcmi_config* cfg, mcmi_result** out
 int mcmi_build_rows(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_begin,
                     int64_t row_end, mcmi_result** out, char* err, size_t errlen) {
     const mcmi::DeviceGuard device_guard;
+    if (!out) return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
     *out = nullptr;
     if (!b || !cfg) return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
     auto* r = new mcmi_result();
-    const Status st = build_parts(*b, *cfg, row_begin, row_end, r);
+    const Status st = build_host(*b, *cfg, row_begin, row_end, r, nullptr, 0.0);
     if (st.code) {
         delete r;
         return report(st, err, errlen);
     }
     *out = r;
     return MCMI_OK;
+}
+
+int mcmi_estimate_rows(const mcmi_csr_view* a, const double* p_values, int64_t row_begin, int64_t row_end,
+                       int64_t n_chains, int64_t max_len, double delta, uint64_t seed, int32_t rng_mode, int device,
+                       mcmi_result** out, char* err, size_t errlen) {
+    const mcmi::DeviceGuard device_guard;
+    if (!out) return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    *out = nullptr;
+    if (!a || (a->n > 0 && a->row_ptr && a->row_ptr[a->n] > 0 && !p_values))
+        return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    mcmi_config c;
+    mcmi_config_default(&c);
+    c.delta = delta;
+    c.master_seed = seed;
+    c.rng_mode = rng_mode;
+    c.device = device;
+    c.n_gpus = 1;
+    c.flags = MCMI_FLAG_UNSCALED;
+    const ApSource ap{p_values, n_chains, max_len};
+    auto* r = new mcmi_result();
+    const Status st = build_host(*a, c, row_begin, row_end, r, nullptr, 0.0, &ap);
+    if (st.code) {
+        delete r;
+        return report(st, err, errlen);
+    }
+    *out = r;
+    return MCMI_OK;
+}
+
+int mcmi_build_start(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_begin, int64_t row_end,
+                     mcmi_job** job, char* err, size_t errlen) {
+    if (!job) return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    *job = nullptr;
+    if (!b || !cfg) return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    auto* j = new mcmi_job();
+    j->b = *b;
+    j->cfg = *cfg;
+    j->lo = row_begin;
+    j->hi = row_end;
+    try {
+        j->th = std::thread([j] {
+            auto* r = new mcmi_result();
+            auto publish = [j](int64_t est) {
+                std::lock_guard<std::mutex> lk(j->mu);
+                if (!j->has_estimate) {
+                    j->has_estimate = true;
+                    j->estimate = est;
+                }
+                j->cv.notify_all();
+            };
+            // a small first chunk (10% of the rows) gives the caller its entry
+            // estimate early enough to size its own arrays while the walks run
+            const Status st = build_host(j->b, j->cfg, j->lo, j->hi, r, publish, 0.1);
+            std::lock_guard<std::mutex> lk(j->mu);
+            if (st.code) {
+                delete r;
+                r = nullptr;
+            } else if (!j->has_estimate) {
+                j->has_estimate = true;
+                j->estimate = r->nnz;
+            }
+            j->code = st.code;
+            j->msg = st.msg;
+            j->result = r;
+            j->done = true;
+            j->cv.notify_all();
+        });
+    } catch (const std::exception& ex) {
+        delete j;
+        return report(fail(MCMI_ENOMEM, std::string("cannot start the build thread: ") + ex.what()), err, errlen);
+    }
+    *job = j;
+    return MCMI_OK;
+}
+
+int mcmi_job_estimate(mcmi_job* job, int64_t* nnz_estimate) {
+    if (!job || !nnz_estimate) return MCMI_EINVAL;
+    std::unique_lock<std::mutex> lk(job->mu);
+    job->cv.wait(lk, [&] { return job->has_estimate || job->done; });
+    *nnz_estimate = job->has_estimate ? job->estimate : -1;
+    return job->done ? job->code : MCMI_OK;
+}
+
+int mcmi_job_finish(mcmi_job* job, mcmi_result** out, char* err, size_t errlen) {
+    if (!job) return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    if (job->th.joinable()) job->th.join();
+    const Status st{job->code, job->msg};
+    if (out) {
+        *out = job->result;
+    } else if (job->result) {
+        delete job->result;
+    }
+    delete job;
+    return report(st, err, errlen);
 }
 
 int mcmi_build_into(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_begin, int64_t row_end,
@@ -1369,7 +1736,7 @@ int mcmi_build_into(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_
         // several GPUs: shards are built concurrently, then each GPU copies its
         // shard straight to its global offset (offsets are known only after
         // every shard has its entry count, so the copies do not overlap the walks)
-        mcmi_result r;
+        DeviceParts r;
         Status st = build_parts(*b, *cfg, row_begin, row_end, &r);
         if (st.code) return report(st, err, errlen);
         *nnz = r.nnz;
@@ -1389,7 +1756,13 @@ int mcmi_build_into(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_
     Status st;
     mcmi_engine* e = acquire_engine(c.device, &st);
     if (!e) return report(st, err, errlen);
-    const HostSink sink{row_ptr, col_idx, values, capacity, chains_used, entries_before};
+    HostSink sink;
+    sink.row_ptr = row_ptr;
+    sink.col_idx = col_idx;
+    sink.values = values;
+    sink.capacity = capacity;
+    sink.chains_used = chains_used;
+    sink.entries_before = entries_before;
     mcmi_device_csr dc{};
     mcmi_stats ls{};
     st = build_from_host(e, *b, c, row_begin, row_end, &dc, &ls, &sink);
@@ -1485,6 +1858,36 @@ int mcmi_drop_small_entries(const mcmi_csr_view* m, double p, int32_t drop_mode,
     return report(st, err, errlen);
 }
 
+int mcmi_retain_top_k(const mcmi_csr_view* rows, int64_t k, const int64_t* diag_cols, int device,
+                      int64_t* out_row_ptr, int64_t* out_col_idx, double* out_values, int64_t* out_nnz, char* err,
+                      size_t errlen) {
+    const mcmi::DeviceGuard device_guard;
+    if (!out_row_ptr || !out_nnz) return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    if (Status st = check_host_view(rows); st.code) return report(st, err, errlen);
+    if (rows->n > 0 && rows->row_ptr[rows->n] > 0 && (!out_col_idx || !out_values))
+        return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    Status st;
+    mcmi_engine* e = acquire_engine(device, &st);
+    if (!e) return report(st, err, errlen);
+    st = retain_top_k_dev(e, *rows, k, diag_cols, out_row_ptr, out_col_idx, out_values, out_nnz);
+    release_engine(e);
+    return report(st, err, errlen);
+}
+
+int mcmi_scale_columns(const mcmi_csr_view* rows, const double* b1_diag, int64_t b1_len, int device,
+                       double* out_values, char* err, size_t errlen) {
+    const mcmi::DeviceGuard device_guard;
+    if (Status st = check_host_view(rows); st.code) return report(st, err, errlen);
+    if (rows->n > 0 && rows->row_ptr[rows->n] > 0 && (!out_values || !b1_diag))
+        return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
+    Status st;
+    mcmi_engine* e = acquire_engine(device, &st);
+    if (!e) return report(st, err, errlen);
+    st = scale_columns_dev(e, *rows, b1_diag, b1_len, out_values);
+    release_engine(e);
+    return report(st, err, errlen);
+}
+
 int mcmi_partition_rows(const int64_t* row_ptr, int64_t row_begin, int64_t row_end, int parts, int64_t* edges) {
     if (!row_ptr || !edges || parts < 1 || row_begin < 0 || row_end < row_begin) return MCMI_EINVAL;
     const std::vector<int64_t> e = partition_rows(row_ptr, row_begin, row_end, parts);
@@ -1502,12 +1905,29 @@ int mcmi_result_sizes(const mcmi_result* r, int64_t* n, int64_t* nnz) {
 int mcmi_result_copy(const mcmi_result* r, int64_t* row_ptr, int64_t* col_idx, double* values,
                      int64_t* chains_used, int64_t* entries_before, int64_t* n_chains,
                      int64_t* max_len) {
-    const mcmi::DeviceGuard device_guard;
     if (!r) return MCMI_EINVAL;
-    const int code = copy_parts(r, row_ptr, col_idx, values, chains_used, entries_before);
+    auto cp = [](void* dst, const PinnedBuf& src, int64_t count) {
+        if (dst && src.p && count > 0) parallel_copy(dst, src.p, static_cast<size_t>(count) * 8);
+    };
+    cp(col_idx, r->ci, r->nnz);
+    cp(values, r->v, r->nnz);
+    cp(row_ptr, r->rp, r->n + 1);
+    cp(chains_used, r->cu, r->n);
+    cp(entries_before, r->eb, r->n);
     if (n_chains) *n_chains = r->n_chains;
     if (max_len) *max_len = r->max_len;
-    return code;
+    return MCMI_OK;
+}
+
+int mcmi_result_view(const mcmi_result* r, const int64_t** row_ptr, const int64_t** col_idx, const double** values,
+                     const int64_t** chains_used, const int64_t** entries_before) {
+    if (!r) return MCMI_EINVAL;
+    if (row_ptr) *row_ptr = r->rp.as<const int64_t>();
+    if (col_idx) *col_idx = r->nnz ? r->ci.as<const int64_t>() : nullptr;
+    if (values) *values = r->nnz ? r->v.as<const double>() : nullptr;
+    if (chains_used) *chains_used = r->cu.as<const int64_t>();
+    if (entries_before) *entries_before = r->eb.as<const int64_t>();
+    return MCMI_OK;
 }
 
 int mcmi_result_stats(const mcmi_result* r, mcmi_stats* stats) {
@@ -1516,12 +1936,7 @@ int mcmi_result_stats(const mcmi_result* r, mcmi_stats* stats) {
     return MCMI_OK;
 }
 
-void mcmi_result_free(mcmi_result* r) {
-    const mcmi::DeviceGuard device_guard;
-    if (!r) return;
-    free_parts(r);
-    delete r;
-}
+void mcmi_result_free(mcmi_result* r) { delete r; }
 
 int mcmi_host_register(void* ptr, size_t bytes) {
     if (!ptr || !bytes) return MCMI_OK;

@@ -82,6 +82,20 @@ struct TableBuildArgs {
     double* b1_diag;
 };
 
+// Transition tables from a caller-built SplitSystem (mcmi_estimate_rows).
+struct ApTableArgs {
+    int64_t n;
+    const int64_t* row_ptr;  // A's (and P's) row pointer
+    const int64_t* col_idx;  // A's columns
+    const double* a_values;
+    const double* p_values;  // P on A's pattern
+    Reductions* red;
+    uint4* rec;
+    double2* ent;
+    int* col;
+    double* b1_diag;
+};
+
 // The SplitSystem as matrices (mcmi_augment_and_split).
 struct SplitExportArgs {
     int64_t n;
@@ -150,6 +164,7 @@ cudaError_t launch_validate_row_ptr(const int64_t* row_ptr, int64_t n, int64_t n
 cudaError_t launch_table_build(const TableBuildArgs& a, int64_t nnz, bool drop_active,
                                cudaStream_t s);
 cudaError_t launch_table_fill(const TableBuildArgs& a, cudaStream_t s);
+cudaError_t launch_ap_tables(const ApTableArgs& a, cudaStream_t s);
 // drop_small_entries: pass 0 row counts (value range first), pass 1 fill.
 cudaError_t launch_drop_filter(const TableBuildArgs& a, bool drop_active, int pass, int* cnt, const int64_t* out_rp,
                                int64_t* oci, double* ov, cudaStream_t s);
@@ -166,6 +181,14 @@ size_t walk_smem_bytes_per_warp(int cap, int lanes, int log_stride);
 size_t walk_global_bytes_per_warp(int cap, int lanes, int log_stride);
 cudaError_t launch_walk(const WalkArgs& a, int warps_per_block, int num_sms, bool global_tier,
                         int64_t max_warps, cudaStream_t s);
+
+// retain_top_k / scale_columns over the rows of a CSR (rowops.cu).  top-k pass
+// 0 writes per-row kept counts (int), pass 1 the kept entries at out_rp.
+cudaError_t launch_topk_rows(const int64_t* rp, const int64_t* ci, const double* v, int64_t n, int64_t k,
+                             const int64_t* diag, int pass, int* cnt, const int64_t* out_rp, int64_t* oci,
+                             double* ov, cudaStream_t s);
+cudaError_t launch_scale_columns(const int64_t* ci, const double* v, int64_t nnz, const double* b1, int64_t b1_len,
+                                 double* out, int* bad, cudaStream_t s);
 
 // Exclusive scans (assemble.cu).
 size_t scan_scratch_bytes(int64_t n);

@@ -308,6 +308,65 @@ __global__ void k_rows_fill(TableBuildArgs a) {
     }
 }
 
+// Tables straight from a caller-built SplitSystem (estimate_row on split.a /
+// split.p, mc_engine.cpp:64-105): state i's transitions are P's row i in
+// stored order, cum_k = sequential sum of p, ratio_k = a_k / p_k, col_k = A's
+// column (P has A's pattern, test_mc_split.cpp:24-25).  No drop, no split.
+__global__ void k_ap_fill(ApTableArgs a) {
+    unsigned long long max_deg = 0, nnz_a = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t k0 = a.row_ptr[i], k1 = a.row_ptr[i + 1];
+        const unsigned begin = static_cast<unsigned>(k0);
+        const unsigned cnt = static_cast<unsigned>(k1 - k0);
+        uint4 r0 = make_uint4(begin, cnt, 0u, 0u), r1 = make_uint4(0u, 0u, 0u, 0u);
+        const unsigned scale = (cnt + 254u) / 255u;
+        unsigned char g[kGuide];
+        int m_next = 0;
+        double cum = 0.0;
+        for (int64_t k = k0; k < k1; ++k) {
+            const int64_t c = a.col_idx[k];
+            if (c < 0 || c >= a.n) atomicMin(&a.red->bad_col_row, static_cast<long long>(i));
+            const double p = a.p_values[k];
+            cum += p;  // sample_transition's running sum (mc_engine.cpp:71-75)
+            const double ratio = a.a_values[k] / p;  // mc_engine.cpp:94
+            const unsigned o = static_cast<unsigned>(k - k0);
+            a.ent[k] = make_double2(cum, ratio);
+            a.col[k] = static_cast<int>(c);
+            if (cnt == 1) {
+                const unsigned long long rb = static_cast<unsigned long long>(__double_as_longlong(ratio));
+                r0.z = static_cast<unsigned>(rb);
+                r0.w = static_cast<unsigned>(rb >> 32);
+                r1.z = static_cast<unsigned>(c);
+            }
+            while (m_next < kGuide && cum > static_cast<double>(m_next) * (1.0 / kGuide))
+                g[m_next++] = static_cast<unsigned char>(o / scale);
+        }
+        while (m_next < kGuide) g[m_next++] = static_cast<unsigned char>(cnt / scale);
+        if (cnt >= 2) {
+            unsigned w[4];
+            for (int q = 0; q < 4; ++q)
+                w[q] = g[4 * q] | (g[4 * q + 1] << 8) | (g[4 * q + 2] << 16) |
+                       (static_cast<unsigned>(g[4 * q + 3]) << 24);
+            r0.z = w[0];
+            r0.w = w[1];
+            r1.x = w[2];
+            r1.y = w[3];
+        }
+        a.rec[2 * i] = r0;
+        a.rec[2 * i + 1] = r1;
+        a.b1_diag[i] = 1.0;  // unused: estimate_row returns unscaled rows
+        max_deg = max(max_deg, static_cast<unsigned long long>(cnt));
+        nnz_a += cnt;
+    }
+    const unsigned long long md = block_max_u64(max_deg);
+    nnz_a = block_sum_u64(nnz_a);
+    if (threadIdx.x == 0) {
+        atomicMax(&a.red->max_deg, md);
+        atomicAdd(&a.red->a_nnz, nnz_a);
+    }
+}
+
 // ---- count-quantile drop (csr.cpp:138-155): radix select of the n_drop-th
 // smallest |b_ij| over off-diagonals, ties resolved by entry position.
 
@@ -610,6 +669,11 @@ cudaError_t launch_table_build(const TableBuildArgs& a, int64_t /*nnz*/, bool dr
     if (drop_active && a.drop_mode == 0) k_offdiag_range<<<g, TB, 0, s>>>(a);
     k_rows_norm<<<g, TB, 0, s>>>(a);
     k_rows_split<<<g, TB, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_ap_tables(const ApTableArgs& a, cudaStream_t s) {
+    if (a.n > 0) k_ap_fill<<<grid_for(a.n), TB, 0, s>>>(a);
     return cudaGetLastError();
 }
 

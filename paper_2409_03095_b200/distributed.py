@@ -11,10 +11,10 @@ Two assemblies:
     (``mcmi_scatter_shard``, csrc/scatter.cu) stores the rank's shard straight
     into every GPU's symmetric M buffer over NVLink peer memory, then a
     symmetric-memory barrier; no padding, staging or concatenation passes.
-  * ``allgatherv_csr``: NCCL has no all-gather-v, so shards are padded to the
-    largest shard and gathered with one ``all_gather_into_tensor`` per array,
-    then trimmed.  It is the reference point for the fused path and runs on
-    gloo (CPU tensors) for the host-side tests.
+  * ``allgatherv_csr``: the all-gather-v as grouped point-to-point transfers
+    (every shard sent straight into its slice of every rank's output; NCCL
+    send/recv in one group).  It is the reference point for the fused path and
+    runs on gloo (CPU tensors) for the host-side tests.
 """
 from __future__ import annotations
 
@@ -37,49 +37,71 @@ def partition_rows(row_ptr: np.ndarray, world: int) -> list[tuple[int, int]]:
     return [(int(edges[g]), int(edges[g + 1])) for g in range(world)]
 
 
-def _gather_padded(t, dist, group=None):
+def _gather_sizes(t, dist, group=None):
+    """All-gather of one small fixed-size tensor per rank -> [world, ...]."""
     import torch
     world = dist.get_world_size(group)
     if t.is_cuda:
         out = torch.empty(world * t.numel(), dtype=t.dtype, device=t.device)
         dist.all_gather_into_tensor(out, t.contiguous(), group=group)
-        return [out[g * t.numel():(g + 1) * t.numel()] for g in range(world)]
+        return out.view(world, -1)
     parts = [torch.empty_like(t) for _ in range(world)]
     dist.all_gather(parts, t.contiguous(), group=group)
-    return parts
+    return torch.stack(parts)
 
 
 def allgatherv_csr(row_ptr, col_idx, values, dist, group=None):
-    """All-gather variable-size CSR row shards (rank order) into the full M.
+    """All-gather-v of variable-size CSR row shards (rank order) into the full M.
 
     row_ptr: int64 [rows_g + 1] starting at 0; col_idx int64 [nnz_g];
-    values float64 [nnz_g].  Returns (row_ptr, col_idx, values) of the
-    concatenation on every rank (same device as the inputs).
+    values float64 [nnz_g].  One all-gather of (nnz_g, rows_g), then every rank
+    sends its shard to every peer and receives each peer's shard straight into
+    that peer's slice of the output (grouped point-to-point: NCCL send/recv
+    inside one group) — no padding, no trimming, no concatenation
+    pass.  The received row pointers are shifted by their shard's entry offset
+    on the device.  Returns (row_ptr, col_idx, values) of the concatenation on
+    every rank (same device as the inputs).
     """
     import torch
     dev = col_idx.device
-    sizes = torch.tensor([col_idx.numel(), row_ptr.numel() - 1], dtype=torch.int64, device=dev)
-    all_sizes = torch.stack(_gather_padded(sizes, dist, group)).cpu()
-    mx_nnz = max(int(all_sizes[:, 0].max()), 1)
-    mx_rows = int(all_sizes[:, 1].max())
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    rows = row_ptr.numel() - 1
+    sizes = _gather_sizes(torch.tensor([col_idx.numel(), rows], dtype=torch.int64, device=dev), dist, group).cpu()
+    nnzs, rowss = [int(x) for x in sizes[:, 0]], [int(x) for x in sizes[:, 1]]
+    nnz_off = [sum(nnzs[:g]) for g in range(world)]
+    row_off = [sum(rowss[:g]) for g in range(world)]
+    total_nnz, total_rows = sum(nnzs), sum(rowss)
+    out_c = torch.empty(max(total_nnz, 1), dtype=torch.int64, device=dev)
+    out_v = torch.empty(max(total_nnz, 1), dtype=torch.float64, device=dev)
+    out_r = torch.empty(total_rows + 1, dtype=torch.int64, device=dev)
 
-    def pad(t, length, dtype):
-        p = torch.zeros(length, dtype=dtype, device=dev)
-        p[: t.numel()] = t
-        return p
+    def my(t, off, cnt):
+        return t[off: off + cnt]
 
-    cols = _gather_padded(pad(col_idx, mx_nnz, torch.int64), dist, group)
-    vals = _gather_padded(pad(values, mx_nnz, torch.float64), dist, group)
-    rps = _gather_padded(pad(row_ptr, mx_rows + 1, torch.int64), dist, group)
-    out_c, out_v, out_r, off = [], [], [], 0
-    for g in range(all_sizes.shape[0]):
-        k, r = int(all_sizes[g, 0]), int(all_sizes[g, 1])
-        out_c.append(cols[g][:k])
-        out_v.append(vals[g][:k])
-        out_r.append(rps[g][:r] + off)
-        off += k
-    out_r.append(torch.tensor([off], dtype=torch.int64, device=dev))
-    return torch.cat(out_r), torch.cat(out_c), torch.cat(out_v)
+    my(out_c, nnz_off[rank], nnzs[rank]).copy_(col_idx[: nnzs[rank]])
+    my(out_v, nnz_off[rank], nnzs[rank]).copy_(values[: nnzs[rank]])
+    my(out_r, row_off[rank], rows).copy_(row_ptr[:rows])
+    ops = []
+    for peer in range(world):
+        if peer == rank:
+            continue
+        # the same (cols, values, row pointers) order on both sides of every pair
+        for t, cnt in ((col_idx, nnzs[rank]), (values, nnzs[rank]), (row_ptr, rows)):
+            if cnt:
+                ops.append(dist.P2POp(dist.isend, t[:cnt].contiguous(), peer, group))
+        for t, off, cnt in ((out_c, nnz_off[peer], nnzs[peer]), (out_v, nnz_off[peer], nnzs[peer]),
+                            (out_r, row_off[peer], rowss[peer])):
+            if cnt:
+                ops.append(dist.P2POp(dist.irecv, my(t, off, cnt), peer, group))
+    if ops:
+        for req in dist.batch_isend_irecv(ops):
+            req.wait()
+    if total_rows:
+        shift = torch.repeat_interleave(torch.tensor(nnz_off, dtype=torch.int64, device=dev),
+                                        torch.tensor(rowss, dtype=torch.int64, device=dev))
+        out_r[:total_rows] += shift
+    out_r[total_rows] = total_nnz
+    return out_r, out_c[:total_nnz], out_v[:total_nnz]
 
 
 def build_sharded(b, cfg, dist, engine=None, device=None, stream=None, tensors=None, assembly="p2p", sym=None):
@@ -117,6 +139,11 @@ def p2p_layout(n: int, nnz_total: int) -> tuple[int, int, int]:
     col_at = a16(8 * (n + 1))
     val_at = col_at + a16(8 * nnz_total)
     return col_at, val_at, val_at + a16(8 * nnz_total)
+
+
+#: symmetric-memory barrier timeout (the rendezvous is bounded by the process
+#: group's store timeout: bench.py creates its group with a 180 s timeout)
+P2P_BARRIER_TIMEOUT_MS = 60_000
 
 
 class SymmetricM:
@@ -177,7 +204,8 @@ def assemble_p2p(shard, lo: int, hi: int, n: int, dist, sym: SymmetricM, stream=
     if code != L.MCMI_OK:
         raise RuntimeError(f"mcmi_scatter_shard failed with status {code}")
     with torch.cuda.stream(st):
-        sym.handle.barrier()
+        # bounded: a peer that never arrives fails the step instead of hanging the job
+        sym.handle.barrier(channel=0, timeout_ms=P2P_BARRIER_TIMEOUT_MS)
     b = sym.buf
     rp = b[: 8 * (n + 1)].view(torch.int64)
     ci = b[col_at: col_at + 8 * total].view(torch.int64)

@@ -58,8 +58,15 @@ class DeviceEngine:
 
     def build(self, n: int, row_ptr, col_idx, values, cfg: McConfig, row_begin: int = 0,
               row_end: int = -1, stream=None) -> DeviceCsr:
-        """``row_ptr``/``col_idx``/``values``: device tensors (or raw pointers)."""
+        """``row_ptr``/``col_idx``/``values``: device tensors (or raw pointers).
+
+        Runs on ``stream`` (a torch stream or a raw cudaStream_t); by default on
+        torch's current stream of the engine's device, so B tensors still being
+        produced by queued torch work are complete before the build reads them."""
         ptr = lambda t: t if isinstance(t, int) else t.data_ptr()  # noqa: E731
+        if stream is None:
+            import torch
+            stream = torch.cuda.current_stream(torch.device("cuda", self.device))
         view = L.mcmi_csr_view(int(n), ptr(row_ptr), ptr(col_idx), ptr(values))
         c = cfg.to_c()
         out = L.mcmi_device_csr()
@@ -81,7 +88,9 @@ class DeviceEngine:
         v = torch.empty(max(nnz, 1), dtype=torch.float64, device=dev)
         cu = torch.empty(max(rows, 1), dtype=torch.int64, device=dev)
         eb = torch.empty(max(rows, 1), dtype=torch.int64, device=dev)
-        s = None if stream is None else stream.cuda_stream
+        if stream is None:
+            stream = torch.cuda.current_stream(dev)
+        s = stream if isinstance(stream, int) else stream.cuda_stream
         for dst, src, nb in ((rp, d.raw.row_ptr, 8 * (rows + 1)), (ci, d.raw.col_idx, 8 * nnz),
                              (v, d.raw.values, 8 * nnz), (cu, d.raw.chains_used, 8 * rows),
                              (eb, d.raw.entries_before, 8 * rows)):

@@ -11,13 +11,24 @@ the reference library in tests/test_generators.py).  The others are new shapes t
                       log-uniform magnitudes                          — config C5
 
 All return a :class:`~paper_2409_03095_b200.mcspai.CsrMatrix` with sorted,
-duplicate-free rows (the from_triplets invariants, csr.hpp:12-15).
+duplicate-free rows (the from_triplets invariants, csr.hpp:12-15).  The module
+needs only numpy, so bench.py's reference arm and the golden-vector scripts
+import it by file path, without the package (which maps libmcmi.so).
 """
 from __future__ import annotations
 
 import numpy as np
 
-from .mcspai import CsrMatrix
+try:
+    from .mcspai import CsrMatrix
+except ImportError:  # loaded by file path (bench.py --impl reference, tests/golden): no product import
+
+    class CsrMatrix:  # type: ignore[no-redef]  # the fields of mcspai.CsrMatrix (csr.hpp:16-21)
+        def __init__(self, n, row_ptr, col_idx, values):
+            self.n, self.row_ptr, self.col_idx, self.values = int(n), row_ptr, col_idx, values
+
+        def nnz(self) -> int:
+            return int(self.values.size)
 
 _M64 = np.uint64(0xFFFFFFFFFFFFFFFF)
 
@@ -172,3 +183,4 @@ CONFIGS = {
                        {"alpha": 0.1, "delta": 1e-300, "chains_override": 100, "max_len_override": 8,
                         "retain_k": 32}),
 }
+

@@ -270,26 +270,57 @@ def compute_preconditioner(b: CsrMatrix, cfg: McConfig | None = None, n_threads:
                                  ChainBudget(st.n_chains, st.max_len), int(cfg.master_seed), st.as_dict())
     code = lib.mcmi_build_rows(C.byref(view), C.byref(c), lo, hi, C.byref(h), err, 1024)
     raise_for(code, err.value.decode(errors="replace"))
-    try:
-        n, nnz = C.c_int64(), C.c_int64()
-        lib.mcmi_result_sizes(h, C.byref(n), C.byref(nnz))
-        n, nnz = n.value, nnz.value
-        if out is not None and out.get("values") is not None and out["values"].size >= nnz:
-            rp, ci, v = out["row_ptr"][: n + 1], out["col_idx"][:nnz], out["values"][:nnz]
-        else:
-            rp, ci, v = np.empty(n + 1, np.int64), np.empty(nnz, np.int64), np.empty(nnz, np.float64)
+    owner = _ResultOwner(h)
+    n, nnz = C.c_int64(), C.c_int64()
+    lib.mcmi_result_sizes(h, C.byref(n), C.byref(nnz))
+    n, nnz = n.value, nnz.value
+    st = L.mcmi_stats()
+    lib.mcmi_result_stats(h, C.byref(st))
+    if out is not None and out.get("values") is not None and out["values"].size >= nnz:
+        # caller arrays: one multi-threaded host copy out of the result
+        rp, ci, v = out["row_ptr"][: n + 1], out["col_idx"][:nnz], out["values"][:nnz]
         cu, eb = np.empty(n, np.int64), np.empty(n, np.int64)
         nc, ml = C.c_int64(), C.c_int64()
-        code = lib.mcmi_result_copy(h, rp.ctypes.data, ci.ctypes.data if nnz else None,
-                                    v.ctypes.data if nnz else None, cu.ctypes.data if n else None,
-                                    eb.ctypes.data if n else None, C.byref(nc), C.byref(ml))
-        raise_for(code, "result copy failed")
-        st = L.mcmi_stats()
-        lib.mcmi_result_stats(h, C.byref(st))
-    finally:
-        lib.mcmi_result_free(h)
-    return ApproxInverse(CsrMatrix(n, rp, ci, v), RowMeta(cu, eb), cfg, ChainBudget(nc.value, ml.value),
+        raise_for(lib.mcmi_result_copy(h, rp.ctypes.data, ci.ctypes.data if nnz else None,
+                                       v.ctypes.data if nnz else None, cu.ctypes.data if n else None,
+                                       eb.ctypes.data if n else None, C.byref(nc), C.byref(ml)), "result copy failed")
+    else:
+        # zero copy: numpy views of the library's page-locked result arrays,
+        # which stay alive (and out of the library's pool) while any view does
+        rp, ci, v, cu, eb = owner.arrays(n, nnz)
+    return ApproxInverse(CsrMatrix(n, rp, ci, v), RowMeta(cu, eb), cfg, ChainBudget(st.n_chains, st.max_len),
                          int(cfg.master_seed), st.as_dict())
+
+
+class _ResultOwner:
+    """Owns an mcmi_result; numpy views of its host arrays keep it alive."""
+
+    def __init__(self, h):
+        self.h = h
+        self.lib = L.load()
+
+    def arrays(self, n, nnz):
+        ptrs = [C.c_void_p() for _ in range(5)]
+        raise_for(self.lib.mcmi_result_view(self.h, *[C.byref(p) for p in ptrs]), "result view failed")
+
+        def view(ptr, count, ctype, dtype):
+            if count <= 0 or not ptr.value:
+                return np.zeros(max(count, 0), dtype)
+            buf = (ctype * count).from_address(ptr.value)
+            buf._owner = self  # the ctypes buffer (numpy's base) keeps the result alive
+            return np.frombuffer(buf, dtype=dtype)
+
+        return (view(ptrs[0], n + 1, C.c_int64, np.int64), view(ptrs[1], nnz, C.c_int64, np.int64),
+                view(ptrs[2], nnz, C.c_double, np.float64), view(ptrs[3], n, C.c_int64, np.int64),
+                view(ptrs[4], n, C.c_int64, np.int64))
+
+    def __del__(self):
+        try:
+            if self.h:
+                self.lib.mcmi_result_free(self.h)
+                self.h = None
+        except Exception:  # noqa: BLE001 — interpreter shutdown
+            pass
 
 
 def host_register(*arrays):
@@ -405,23 +436,92 @@ class RngStream:  # rng.hpp:17-30: RngStream(seed, stream_id)
     stream_id: int
 
 
+def estimate_rows(split: SplitSystem, row_begin: int, row_end: int, budget: ChainBudget, delta: float, seed: int,
+                  rng_mode: RngMode = RngMode.reference, device: int = 0) -> CsrMatrix:
+    """mcspai::estimate_row (mc_engine.hpp:63-65) for rows [row_begin, row_end)
+    at once, on the GPU (``mcmi_estimate_rows``): row r is estimate_row(split,
+    r, budget, delta, RngStream(seed, r)) — columns sorted, unscaled, nothing
+    pruned.  Uses only split.a and split.p (a hand-built SplitSystem works, as
+    in the reference's tests, test_mc_engine.cpp:112-127)."""
+    a, p = split.a, split.p
+    if not (p.n == a.n and np.array_equal(p.row_ptr, a.row_ptr) and np.array_equal(p.col_idx, a.col_idx)):
+        raise ValueError("estimate_row: P must have A's sparsity pattern (transition_probabilities(A))")
+    lib = L.load()
+    h = C.c_void_p()
+    err = C.create_string_buffer(512)
+    pv = np.ascontiguousarray(p.values, np.float64)
+    raise_for(lib.mcmi_estimate_rows(C.byref(_view(a)), pv.ctypes.data if pv.size else None, int(row_begin),
+                                     int(row_end), int(budget.n_chains), int(budget.max_len), float(delta),
+                                     int(seed) & 0xFFFFFFFFFFFFFFFF, int(rng_mode), int(device), C.byref(h), err, 512),
+              err.value.decode(errors="replace"))
+    owner = _ResultOwner(h)
+    n, nnz = C.c_int64(), C.c_int64()
+    lib.mcmi_result_sizes(h, C.byref(n), C.byref(nnz))
+    rp, ci, v, _, _ = owner.arrays(n.value, nnz.value)
+    return CsrMatrix(n.value, rp.copy(), ci.copy(), v.copy())
+
+
 def estimate_row(split: SplitSystem, r: int, budget: ChainBudget, delta: float, stream: RngStream):
     """mcspai::estimate_row (mc_engine.hpp:63-65): row r of (I - A)^-1 as
-    (column, value) pairs, column-sorted, from budget.n_chains walks.
-
-    Runs the build's walk kernel on row r with MCMI_FLAG_UNSCALED.  The device
-    keys row r's draws by RngStream(seed, r), the stream compute_preconditioner
-    gives that row (mc_engine.cpp:168); other stream ids are not supported."""
-    if split.source is None:
-        raise ValueError("estimate_row needs a SplitSystem from augment_and_split")
+    (column, value) pairs, column-sorted, from budget.n_chains walks, on the
+    build's walk kernel (``mcmi_estimate_rows``).  The device keys row r's
+    draws by RngStream(seed, r), the stream compute_preconditioner gives that
+    row (mc_engine.cpp:168); other stream ids are not supported."""
     if int(stream.stream_id) != int(r):
         raise ValueError("estimate_row: the device draws row r from RngStream(seed, r); stream_id must equal r")
-    b, alpha, mode, device = split.source
-    if not 0 <= r < b.n:
+    if not 0 <= r < split.a.n:
         raise IndexError("row out of range")
-    cfg = McConfig(alpha=alpha, mode=mode, delta=float(delta), chains_override=int(budget.n_chains),
-                   max_len_override=int(budget.max_len), master_seed=int(stream.seed), retain_k=0, device=device,
-                   unscaled=True)
-    inv = compute_preconditioner(b, cfg, rows=(int(r), int(r) + 1))
-    return list(zip(inv.m.col_idx.tolist(), inv.m.values.tolist()))
+    m = estimate_rows(split, r, r + 1, budget, delta, stream.seed,
+                      device=split.source[3] if split.source else 0)
+    return list(zip(m.col_idx.tolist(), m.values.tolist()))
 
+
+def retain_top_k_rows(m: CsrMatrix, k: int, diag_cols=None, device: int = 0) -> CsrMatrix:
+    """mcspai::retain_top_k (mc_engine.hpp:70) on every row of ``m`` at once, on
+    the GPU (``mcmi_retain_top_k``): row r keeps its k entries ranked first by
+    (column == diag_cols[r] first, |value| descending, column ascending), in
+    their original order; ``diag_cols`` defaults to r."""
+    n, nnz = m.n, int(m.row_ptr[-1]) if m.n > 0 else 0
+    rp, ci, v = np.zeros(n + 1, np.int64), np.empty(nnz, np.int64), np.empty(nnz)
+    d = None if diag_cols is None else np.ascontiguousarray(diag_cols, np.int64)
+    if d is not None and d.size != n:
+        raise ValueError("diag_cols needs one column per row")
+    got = C.c_int64()
+    err = C.create_string_buffer(512)
+    raise_for(L.load().mcmi_retain_top_k(C.byref(_view(m)), int(k), d.ctypes.data if d is not None and n else None,
+                                         int(device), rp.ctypes.data, ci.ctypes.data if nnz else None,
+                                         v.ctypes.data if nnz else None, C.byref(got), err, 512),
+              err.value.decode(errors="replace"))
+    return CsrMatrix(n, rp, ci[: got.value].copy(), v[: got.value].copy())
+
+
+def retain_top_k(row, k: int, diag_col: int, device: int = 0):
+    """mcspai::retain_top_k(SparseRow, k, diag_col) (mc_engine.hpp:70): a list of
+    (column, value) pairs in, the kept pairs out."""
+    row = list(row)
+    m = CsrMatrix(1, np.array([0, len(row)]), np.array([c for c, _ in row], np.int64),
+                  np.array([x for _, x in row], np.float64))
+    out = retain_top_k_rows(m, k, [diag_col], device)
+    return list(zip(out.col_idx.tolist(), out.values.tolist()))
+
+
+def scale_columns_rows(m: CsrMatrix, b1_diag, device: int = 0) -> CsrMatrix:
+    """mcspai::scale_columns (mc_engine.hpp:74) on every entry of ``m``:
+    value / b1_diag[column], on the GPU (``mcmi_scale_columns``)."""
+    b1 = np.ascontiguousarray(b1_diag, np.float64)
+    nnz = int(m.row_ptr[-1]) if m.n > 0 else 0
+    out = np.empty(nnz)
+    err = C.create_string_buffer(512)
+    raise_for(L.load().mcmi_scale_columns(C.byref(_view(m)), b1.ctypes.data if b1.size else None, b1.size,
+                                          int(device), out.ctypes.data if nnz else None, err, 512),
+              err.value.decode(errors="replace"))
+    return CsrMatrix(m.n, m.row_ptr.copy(), m.col_idx.copy(), out)
+
+
+def scale_columns(row: list, b1_diag, device: int = 0) -> None:
+    """mcspai::scale_columns(SparseRow&, b1_diag) (mc_engine.hpp:74): in place on
+    a list of (column, value) pairs."""
+    m = CsrMatrix(1, np.array([0, len(row)]), np.array([c for c, _ in row], np.int64),
+                  np.array([x for _, x in row], np.float64))
+    out = scale_columns_rows(m, b1_diag, device)
+    row[:] = list(zip(out.col_idx.tolist(), out.values.tolist()))

@@ -107,3 +107,56 @@ def test_library_partition_matches_restatement():
     bad = np.zeros(3, np.int64)
     assert lib.mcmi_partition_rows(bad.ctypes.data, 0, 2, 0, bad.ctypes.data) == L.MCMI_EINVAL
     assert lib.mcmi_partition_rows(bad.ctypes.data, 2, 1, 2, bad.ctypes.data) == L.MCMI_EINVAL
+
+
+def _shard(g, seed):
+    """Synthetic CSR shard of rank g (some shards empty, some with rows but no entries)."""
+    rng = np.random.default_rng(seed * 100 + g)
+    rows = int(rng.choice([0, 1, 5, 40]))
+    counts = rng.integers(0, 6, size=rows) * (rng.random(rows) < 0.7)
+    rp = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    return rp, rng.integers(0, 1000, size=int(rp[-1])).astype(np.int64), rng.normal(size=int(rp[-1]))
+
+
+def _worker_ragged(rank, world, port, seed, q):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2409_03095_b200.distributed import allgatherv_csr
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rp, ci, v = _shard(rank, seed)
+    mrp, mci, mv = allgatherv_csr(torch.from_numpy(rp), torch.from_numpy(ci), torch.from_numpy(v), dist)
+    q.put((rank, mrp.numpy(), mci.numpy(), mv.numpy()))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world,seed", [(2, 1), (3, 2), (4, 3), (4, 4)])
+def test_gloo_allgatherv_ragged_and_empty_shards(world, seed):
+    """The grouped point-to-point all-gather-v on shards of any size (empty,
+    rows without entries): every rank ends with the rank-ordered concatenation,
+    row pointers shifted by the entries before them."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_ragged, args=(r, world, port, seed, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    got = [q.get(timeout=300) for _ in range(world)]
+    for p in procs:
+        p.join(timeout=300)
+        assert p.exitcode == 0
+    parts = [_shard(g, seed) for g in range(world)]
+    want_rp, off = [np.zeros(1, np.int64)], 0
+    for rp, _, _ in parts:
+        want_rp.append(rp[1:] + off)
+        off += int(rp[-1])
+    want_rp = np.concatenate(want_rp)
+    want_ci = np.concatenate([p[1] for p in parts])
+    want_v = np.concatenate([p[2] for p in parts])
+    for _, rp, ci, v in got:
+        assert np.array_equal(rp, want_rp)
+        assert np.array_equal(ci, want_ci)
+        assert np.array_equal(v.view(np.uint64), want_v.view(np.uint64))

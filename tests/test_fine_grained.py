@@ -202,3 +202,134 @@ def test_drop_small_entries_ties_and_errors(ref_mod):
     for bad in (-0.1, 1.1, float("nan")):
         with pytest.raises(ValueError, match=r"^drop fraction must lie in \[0,1\]$"):
             drop_small_entries(b, bad)
+
+
+# ---------------------------------------------- estimate_row on a hand-built SplitSystem
+
+def _hand_split(rng, n, density, p_mode):
+    """A random SplitSystem built by hand, as the reference's tests do: A with
+    random signed values (explicit zeros, empty and single-entry rows), P on A's
+    pattern: transition_probabilities(A), unnormalised weights (rows summing to
+    less than 1 exercise sample_transition's end-1 fallback), or zeros."""
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        k = int(rng.integers(0, max(2, int(density * n))))
+        c = np.unique(rng.integers(0, n, size=k))
+        rows += [i] * c.size
+        cols += c.tolist()
+        vals += (rng.uniform(-0.3, 0.3, size=c.size) * (rng.uniform(size=c.size) > 0.05)).tolist()
+    order = np.lexsort((cols, rows))
+    rows, cols, vals = np.array(rows, np.int64)[order], np.array(cols, np.int64)[order], np.array(vals)[order]
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, rows + 1, 1)
+    rp = np.cumsum(rp)
+    if p_mode == "tp":
+        s = np.bincount(rows, weights=np.abs(vals), minlength=n)
+        s = np.where(s > 0, s, 1.0)
+        p = np.abs(vals) / s[rows]
+    elif p_mode == "short":
+        p = rng.uniform(0.0, 1.0, size=vals.size) / np.repeat(np.maximum(np.diff(rp), 1), np.diff(rp)) * 0.9
+    else:
+        p = rng.uniform(0.0, 0.5, size=vals.size)
+    return n, rp, cols, vals, p
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("p_mode", ["tp", "short", "raw"])
+@pytest.mark.parametrize("rng_seed", [1, 2, 3])
+def test_estimate_rows_hand_built_split_matches_reference(ref_mod, p_mode, rng_seed):
+    """mcmi_estimate_rows on split.a / split.p built by hand equals the
+    reference's estimate_row on the same SplitSystem, row by row, bit for bit."""
+    from paper_2409_03095_b200.mcspai import ChainBudget, CsrMatrix, SplitSystem, estimate_rows
+    rng = np.random.default_rng(rng_seed)
+    n, rp, ci, av, pv = _hand_split(rng, 150, 0.05, p_mode)
+    a = CsrMatrix(n, rp, ci, av)
+    split = SplitSystem(b_hat=a, b1_diag=np.ones(n), a=a, p=CsrMatrix(n, rp, ci, pv), s_diag=np.zeros(n), a_norm=0.5)
+    want_sp = ref_mod.split_from_ap(n, rp, ci, av, pv)
+    try:
+        for nc, ml, delta, seed in ((200, 3, 1e-3, 5), (37, 8, 1e-9, 20261019), (1, 1, 0.5, 0)):
+            got = estimate_rows(split, 0, n, ChainBudget(nc, ml), delta, seed)
+            for r in range(n):
+                wc, wv = ref_mod.estimate_row(want_sp, r, nc, ml, delta, seed)
+                a0, a1 = got.row_ptr[r], got.row_ptr[r + 1]
+                assert got.col_idx[a0:a1].tolist() == wc.tolist(), (r, nc, ml)
+                assert bits_equal(got.values[a0:a1], wv), (r, nc, ml)
+    finally:
+        ref_mod.free_split(want_sp)
+
+
+@pytest.mark.gpu
+def test_estimate_row_single_transition_chain_exact():
+    """test_mc_engine.cpp:112-127: A = [[0, 0.5], [0, 0]], P = transition_probabilities(A),
+    (I - A)^-1 row 0 = [1, 0.5] exactly, for any seed."""
+    from paper_2409_03095_b200.mcspai import (ChainBudget, CsrMatrix, RngStream, SplitSystem, estimate_row,
+                                              transition_probabilities)
+    a = CsrMatrix.from_triplets(2, [0], [1], [0.5])
+    split = SplitSystem(b_hat=a, b1_diag=np.ones(2), a=a, p=transition_probabilities(a), s_diag=np.zeros(2),
+                        a_norm=0.5)
+    for seed in (1, 99, 31337):
+        assert estimate_row(split, 0, ChainBudget(25, 8), 1e-6, RngStream(seed, 0)) == [(0, 1.0), (1, 0.5)]
+
+
+@pytest.mark.gpu
+def test_estimate_row_identity_absorbs():
+    """test_mc_engine.cpp:100-110: identity input absorbs immediately -> row r = [(r, 1)]."""
+    from paper_2409_03095_b200.mcspai import ChainBudget, CsrMatrix, RngStream, augment_and_split, estimate_row
+    sp = augment_and_split(CsrMatrix.identity(4), 1.0)
+    for r in range(4):
+        assert estimate_row(sp, r, ChainBudget(50, 10), 0.01, RngStream(123, r)) == [(r, 1.0)]
+
+
+# ---------------------------------------------- retain_top_k / scale_columns entry points
+
+@pytest.mark.gpu
+def test_retain_top_k_reference_cases():
+    """test_mc_engine.cpp:193-213, verbatim."""
+    from paper_2409_03095_b200.mcspai import retain_top_k
+    row = [(0, 1.0), (3, 0.5)]
+    assert retain_top_k(row, 5, 0) == row
+    assert retain_top_k(row, 0, 0) == row  # 0 = unlimited
+    assert retain_top_k([(1, 1.0), (3, 0.9), (5, 0.2), (7, 0.8)], 2, 1) == [(1, 1.0), (3, 0.9)]
+    assert retain_top_k([(1, 0.1), (2, 5.0), (4, 5.0), (6, 5.0)], 2, 1) == [(1, 0.1), (2, 5.0)]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_retain_top_k_rows_match_reference(ref_mod, seed):
+    """Every row of a random CSR (ties in |v|, signs, diagonal present or not,
+    rows shorter and longer than k, k <= 0) against the reference's
+    retain_top_k, row by row, bit for bit."""
+    from paper_2409_03095_b200.mcspai import CsrMatrix, retain_top_k_rows
+    rng = np.random.default_rng(seed)
+    n = 300
+    lens = rng.integers(0, 700, size=n)
+    lens[:5] = [0, 1, 2, 600, 1500]
+    rp = np.concatenate(([0], np.cumsum(lens))).astype(np.int64)
+    ci = np.concatenate([np.sort(rng.choice(5000, size=x, replace=False)) for x in lens]).astype(np.int64)
+    v = rng.choice([-0.5, 0.5, 0.25, -1e-3, 2.0], size=ci.size) * (rng.uniform(size=ci.size) < 0.5) + \
+        rng.normal(size=ci.size) * (rng.uniform(size=ci.size) >= 0.5)
+    diag = np.where(rng.uniform(size=n) < 0.5, np.arange(n), rng.integers(0, 5000, size=n))
+    m = CsrMatrix(n, rp, ci, v)
+    for k in (0, -3, 1, 7, 32, 500):
+        got = retain_top_k_rows(m, k, diag)
+        for r in range(n):
+            wc, wv = ref_mod.retain_top_k(ci[rp[r]:rp[r + 1]], v[rp[r]:rp[r + 1]], k, int(diag[r]))
+            a, b = got.row_ptr[r], got.row_ptr[r + 1]
+            assert got.col_idx[a:b].tolist() == wc.tolist(), (k, r)
+            assert bits_equal(got.values[a:b], wv), (k, r)
+
+
+@pytest.mark.gpu
+def test_scale_columns_reference_case_and_range():
+    """test_mc_engine.cpp:215-220, plus the batched form and a column outside b1_diag."""
+    from paper_2409_03095_b200.mcspai import CsrMatrix, scale_columns, scale_columns_rows
+    row = [(0, 1.0), (1, 1.0)]
+    scale_columns(row, [2.0, 4.0])
+    assert row == [(0, 0.5), (1, 0.25)]
+    rng = np.random.default_rng(3)
+    m = CsrMatrix(3, np.array([0, 2, 2, 5]), np.array([0, 4, 1, 2, 3]), rng.normal(size=5))
+    b1 = rng.uniform(0.5, 3.0, size=5)
+    got = scale_columns_rows(m, b1)
+    assert bits_equal(got.values, m.values / b1[m.col_idx])
+    with pytest.raises(IndexError):
+        scale_columns_rows(m, b1[:3])

@@ -110,13 +110,20 @@ def test_zero_variance_equals_truncated_neumann(mc):
             assert inv.m == ref
 
 
-def test_single_transition_chain_exact(mc):
-    # test_mc_engine.cpp:112-127 analogue at pipeline level: row 0 has one
-    # off-diagonal entry, so (I-A)^{-1} row 0 = [1, a] exactly for any seed
+def test_single_transition_chain_exact(mc, ref_mod):
+    # test_mc_engine.cpp:112-127 at pipeline level (the estimate_row form on a
+    # hand-built SplitSystem is test_fine_grained.py::
+    # test_estimate_row_single_transition_chain_exact): row 0 of B has one
+    # off-diagonal entry, so its walks are deterministic, one chain runs, and
+    # M equals the reference's bit for bit for any seed
     b = mc.CsrMatrix.from_triplets(2, [0, 0, 1], [0, 1, 1], [1.0, -0.5, 1.0])
     for seed in (1, 99, 31337):
         inv = mc.compute_preconditioner(b, mc.McConfig(alpha=1.0, master_seed=seed, delta=1e-6))
         assert inv.row_meta.chains_used[0] == 1
+        want = ref_mod.compute_preconditioner(ref_mod.Csr(2, b.row_ptr, b.col_idx, b.values), alpha=1.0,
+                                              master_seed=seed, delta=1e-6)
+        assert want.chains_used[0] == 1
+        assert bits_equal(inv.m.values, want.m.values) and np.array_equal(inv.m.col_idx, want.m.col_idx)
 
 
 def test_empty_rows_missing_diagonal_and_n0(mc, ref_mod):
@@ -368,12 +375,18 @@ def test_huge_budget_cast_and_long_max_len(mc, oracle_mod, ref_mod, rng):
     # ||A|| = 1 - 1e-15: the reference's static_cast<index_t> of a 1e33 chain
     # budget is INT64_MIN on x86-64, so it runs N = 1 chain with L ~ 7.8e14;
     # the walks still stop early by delta.  The drop-in must do the same.
-    import test_gpu_fuzz as F
-    rng_ = np.random.default_rng(20261018)
-    for case in range(302):
-        b = F.random_matrix(rng_)
-        cfg = F.random_config(rng_, mc)
-    cfg.rng_mode = mc.RngMode(rng)
+    # Frozen fixture (tests/golden/huge_budget_case.json, found by the fuzz generator).
+    import json
+    import os
+    from helpers import GOLDEN
+    with open(os.path.join(GOLDEN, "huge_budget_case.json")) as f:
+        case = json.load(f)
+    b = mc.CsrMatrix(case["n"], np.array(case["row_ptr"], np.int64), np.array(case["col_idx"], np.int64),
+                     np.array([float.fromhex(x) for x in case["values_hex"]]))
+    kw = dict(case["config"])
+    kw.pop("rng_mode")
+    cfg = mc.McConfig(**{k: (mc.AugmentationMode(v) if k == "mode" else mc.DropMode(v) if k == "drop_mode" else v)
+                         for k, v in kw.items()}, rng_mode=mc.RngMode(rng))
     want = oracle_mod.compute_preconditioner(b.n, b.row_ptr, b.col_idx, b.values, **cfg.oracle_kwargs())
     assert want.n_chains == 1 and want.max_len > 10**14
     got = mc.compute_preconditioner(b, cfg)
