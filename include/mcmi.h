@@ -244,7 +244,14 @@ typedef struct mcmi_job mcmi_job;
 int mcmi_build_start(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_begin, int64_t row_end,
                      mcmi_job** job, char* err, size_t errlen);
 int mcmi_job_estimate(mcmi_job* job, int64_t* nnz_estimate);
-int mcmi_job_finish(mcmi_job* job, mcmi_result** out, char* err, size_t errlen);
+/* Hands the job the caller's entry arrays (capacity entries each, once per
+ * job): from then on every row chunk is copied into them as soon as its
+ * device->host copy completes, while later chunks still walk.  Entries beyond
+ * `capacity` are not delivered (mcmi_result_copy_range copies them later). */
+int mcmi_job_attach(mcmi_job* job, int64_t* col_idx, double* values, int64_t capacity);
+/* *delivered (may be NULL) = the leading entries already in the attached
+ * arrays; the rest is copied with mcmi_result_copy_range. */
+int mcmi_job_finish(mcmi_job* job, mcmi_result** out, int64_t* delivered, char* err, size_t errlen);
 
 int mcmi_result_sizes(const mcmi_result* r, int64_t* n, int64_t* nnz);
 /* Any pointer may be NULL.  row_ptr[n+1], col_idx[nnz], values[nnz],
@@ -253,6 +260,9 @@ int mcmi_result_sizes(const mcmi_result* r, int64_t* n, int64_t* nnz);
 int mcmi_result_copy(const mcmi_result* r, int64_t* row_ptr, int64_t* col_idx, double* values,
                      int64_t* chains_used, int64_t* entries_before, int64_t* n_chains,
                      int64_t* max_len);
+/* Entries [begin, end) of col_idx / values (either may be NULL) into
+ * col_idx[begin..end) / values[begin..end): a multi-threaded host copy. */
+int mcmi_result_copy_range(const mcmi_result* r, int64_t begin, int64_t end, int64_t* col_idx, double* values);
 /* Borrowed pointers to the result's host arrays (valid until mcmi_result_free;
  * col_idx / values are NULL when nnz == 0): zero-copy access for bindings. */
 int mcmi_result_view(const mcmi_result* r, const int64_t** row_ptr, const int64_t** col_idx, const double** values,

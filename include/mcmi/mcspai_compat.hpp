@@ -115,9 +115,10 @@ void presize(VecT& v, size_t count) {
 // a library thread (mcmi_build_start) and streams M into page-locked memory
 // chunk by chunk; as soon as the first row chunk gives an entry estimate
 // (mcmi_job_estimate), two host threads size the caller's std::vectors while
-// the GPU keeps walking, so only the final multi-threaded copy out of the
-// library's buffers follows the build.  An estimate that falls short just
-// costs a regrow; the result never depends on it.
+// the GPU keeps walking, then the vectors are attached (mcmi_job_attach) and
+// every chunk is copied into them as it lands, so only the last chunks' copy
+// follows the build.  An estimate that falls short just costs a regrow; the
+// result never depends on it.
 template <class ApproxInverseT, class SplitErrorT, class CsrT, class CfgT>
 ApproxInverseT compute_preconditioner(const CsrT& b, const CfgT& cfg, const Options& opt = {}) {
     const mcmi_config c = to_config(cfg, opt);
@@ -148,13 +149,20 @@ ApproxInverseT compute_preconditioner(const CsrT& b, const CfgT& cfg, const Opti
     } catch (...) {
         for (auto& t : sizers)
             if (t.joinable()) t.join();
-        mcmi_job_finish(job, nullptr, nullptr, 0);
+        mcmi_job_finish(job, nullptr, nullptr, nullptr, 0);
         throw;
     }
-    mcmi_result* res = nullptr;
-    code = mcmi_job_finish(job, &res, err, sizeof err);
+    bool sized = sizers[0].joinable() && sizers[1].joinable();
     for (auto& t : sizers)
         if (t.joinable()) t.join();
+    // the vectors are sized: chunks that already landed, and every later one,
+    // are copied into them while the walks go on
+    if (sized && out.m.col_idx.size() == static_cast<size_t>(est) && out.m.values.size() == static_cast<size_t>(est))
+        sized = mcmi_job_attach(job, reinterpret_cast<int64_t*>(out.m.col_idx.data()), out.m.values.data(), est) ==
+                MCMI_OK;
+    mcmi_result* res = nullptr;
+    int64_t delivered = 0;
+    code = mcmi_job_finish(job, &res, &delivered, err, sizeof err);
     if (code != MCMI_OK) rethrow<SplitErrorT>(code, err);
     struct Guard {
         mcmi_result* r;
@@ -162,6 +170,7 @@ ApproxInverseT compute_preconditioner(const CsrT& b, const CfgT& cfg, const Opti
     } guard{res};
     int64_t n = 0, nnz = 0;
     mcmi_result_sizes(res, &n, &nnz);
+    if (!sized) delivered = 0;
     out.m.n = n;
     out.m.row_ptr.resize(static_cast<size_t>(n) + 1);
     out.m.col_idx.resize(static_cast<size_t>(nnz));  // shrinks in place when the estimate held
@@ -169,9 +178,10 @@ ApproxInverseT compute_preconditioner(const CsrT& b, const CfgT& cfg, const Opti
     chains.resize(static_cast<size_t>(n));
     before.resize(static_cast<size_t>(n));
     int64_t n_chains = 0, max_len = 0;
-    if (mcmi_result_copy(res, reinterpret_cast<int64_t*>(out.m.row_ptr.data()),
-                         reinterpret_cast<int64_t*>(out.m.col_idx.data()), out.m.values.data(),
-                         chains.data(), before.data(), &n_chains, &max_len) != MCMI_OK)
+    if (mcmi_result_copy(res, reinterpret_cast<int64_t*>(out.m.row_ptr.data()), nullptr, nullptr, chains.data(),
+                         before.data(), &n_chains, &max_len) != MCMI_OK ||
+        mcmi_result_copy_range(res, delivered, nnz, reinterpret_cast<int64_t*>(out.m.col_idx.data()),
+                               out.m.values.data()) != MCMI_OK)
         throw std::runtime_error("mcmi: result copy failed");
     out.row_meta.resize(static_cast<size_t>(n));
     for (int64_t i = 0; i < n; ++i) {

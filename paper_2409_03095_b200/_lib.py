@@ -26,7 +26,7 @@ EXPORTS = [
     "mcmi_recover_inverse_device", "mcmi_scatter_shard", "mcmi_derive_chain_budget", "mcmi_augment_and_split",
     "mcmi_split_sizes", "mcmi_split_copy", "mcmi_split_free", "mcmi_transition_probabilities", "mcmi_drop_small_entries",
     "mcmi_build_start", "mcmi_job_estimate", "mcmi_job_finish", "mcmi_result_view", "mcmi_estimate_rows",
-    "mcmi_retain_top_k", "mcmi_scale_columns",
+    "mcmi_retain_top_k", "mcmi_scale_columns", "mcmi_job_attach", "mcmi_result_copy_range",
 ]
 
 
@@ -154,7 +154,9 @@ def load(path: str | None = None):
     L.mcmi_estimate_rows.argtypes = [C.POINTER(mcmi_csr_view), C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
                                      C.c_int64, C.c_double, C.c_uint64, C.c_int32, C.c_int, C.POINTER(C.c_void_p),
                                      C.c_char_p, C.c_size_t]
-    L.mcmi_job_finish.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), C.c_char_p, C.c_size_t]
+    L.mcmi_job_finish.argtypes = [C.c_void_p, C.POINTER(C.c_void_p), _i64p, C.c_char_p, C.c_size_t]
+    L.mcmi_job_attach.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64]
+    L.mcmi_result_copy_range.argtypes = [C.c_void_p, C.c_int64, C.c_int64, C.c_void_p, C.c_void_p]
     L.mcmi_result_stats.argtypes = [C.c_void_p, C.POINTER(mcmi_stats)]
     L.mcmi_result_free.argtypes = [C.c_void_p]
     L.mcmi_result_free.restype = None

@@ -31,6 +31,21 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
     return c;
 }
 
+// The same with the 10 round keys precomputed (rk[2r], rk[2r+1] = key + r *
+// Weyl steps): passed as kernel parameters they become constant-bank operands
+// of the XORs, so a call is 20 IMAD.WIDE + 20 LOP3 with no key updates.
+__device__ __forceinline__ uint4 philox4x32_10_rk(uint4 c, const uint32_t* rk) {
+#pragma unroll
+    for (int round = 0; round < 10; ++round) {
+        const uint32_t lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x);
+        const uint32_t lo1 = 0xCD9E8D57u * c.z;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z);
+        c = make_uint4(hi1 ^ c.y ^ rk[2 * round], lo1, hi0 ^ c.w ^ rk[2 * round + 1], lo0);
+    }
+    return c;
+}
+
 // RngStream::next_double (rng.hpp:32-41): lo word drawn first, 53 bits.
 __device__ __forceinline__ double u32pair_to_double(uint32_t lo, uint32_t hi) {
     const unsigned long long u = (static_cast<unsigned long long>(hi) << 32) | lo;

@@ -13,6 +13,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <condition_variable>
 #include <functional>
 #include <mutex>
@@ -163,6 +164,7 @@ struct mcmi_engine {
     DevBuf red, diag_val, a_cnt, a_off, keep, rec, ent, colA, b1, scan_tmp, cq_tmp;
     DevBuf stage_col, stage_val, row_cnt, row_src, chains_used, entries_before, counters;
     DevBuf ovf[2];
+    DevBuf tri;  // L = 2 split-fold row flags
     DevBuf gscratch;  // global accumulator tier
     DevBuf out_rp, out_col, out_val;
     // streamed build (mcmi_build_into): double-buffered output slabs + copy stream
@@ -231,7 +233,7 @@ void engine_release(mcmi_engine* e) {
     for (DevBuf* b : {&e->red, &e->diag_val, &e->a_cnt, &e->a_off, &e->keep, &e->rec, &e->ent,
                       &e->colA, &e->b1, &e->scan_tmp, &e->cq_tmp, &e->stage_col, &e->stage_val,
                       &e->row_cnt, &e->row_src, &e->chains_used, &e->entries_before,
-                      &e->counters, &e->ovf[0], &e->ovf[1], &e->gscratch, &e->out_rp, &e->out_col,
+                      &e->counters, &e->ovf[0], &e->ovf[1], &e->tri, &e->gscratch, &e->out_rp, &e->out_col,
                       &e->out_val, &e->col_slab[0], &e->col_slab[1],
                       &e->val_slab[0], &e->val_slab[1]})
         b->release();
@@ -299,6 +301,8 @@ struct HostSink {
     std::function<Status(HostSink&, int64_t need, int64_t estimate, int64_t have)> grow;
     // After each row chunk's entry count is known: (rows done, entries so far, rows).
     std::function<void(int64_t, int64_t, int64_t)> progress;
+    // After a chunk's entries [lo, hi) are queued for copy on stream `copy`.
+    std::function<void(int64_t lo, int64_t hi, cudaStream_t copy)> queued;
     double first_chunk = 0.0;  // > 0: fraction of the rows in the first chunk (an early estimate)
 };
 
@@ -490,6 +494,15 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         if (cfg.retain_k > 0) sst = std::min<int64_t>(sst, cfg.retain_k);
         return std::max<int64_t>(sst, 1);
     };
+    // L = 2: flag the rows whose walks can use the split fold (walk.cu); the
+    // test is O(deg^2 deg_j) per row, so only for matrices of small degree
+    const unsigned char* tri = nullptr;
+    if (L == 2 && n > 0 && dmax <= 16 && !getenv("MCMI_WALK_NO_SPLIT")) {
+        MCMI_TRY(e->tri.ensure(n1), "alloc tri");
+        MCMI_TRY(launch_tri_free(e->rec.as<uint4>(), e->colA.as<int>(), n, e->tri.as<unsigned char>(), s), "tri");
+        st.launches += 1;
+        tri = e->tri.as<unsigned char>();
+    }
     int64_t pool_used = 0;
     int cur = 0;
     unsigned long long total_steps = 0, total_deg = 0;
@@ -509,11 +522,18 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
                  "alloc staging");
         MCMI_TRY(cudaMemsetAsync(e->counters.p, 0, 8 * sizeof(unsigned long long), s), "memset");
         WalkArgs wa{};
-        wa.t = Tables{n, e->rec.as<uint4>(), e->ent.as<double2>(), e->colA.as<int>(), e->b1.as<double>()};
+        wa.t = Tables{n, e->rec.as<uint4>(), e->ent.as<double2>(), e->colA.as<int>(), e->b1.as<double>(), tri};
         wa.row_begin = row_begin;
         wa.row_list = row_list;
         wa.work_offset = offset;
         wa.n_work = work;
+        {  // MCMI_WALK_CLAIM: rows per cursor claim (tuning); retries (row lists) claim one at a time
+            static const int claim = [] {
+                const char* v = getenv("MCMI_WALK_CLAIM");
+                return v && *v ? std::max(1, std::min(64, atoi(v))) : 1;
+            }();
+            wa.claim_rows = row_list ? 1 : claim;
+        }
         wa.n_chains = N;
         wa.max_len = std::clamp<int64_t>(L, 0, INT_MAX);  // walks beyond the log capacity overflow anyway
         wa.delta = cfg.delta;
@@ -753,8 +773,8 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
                                     e->out_val.as<double>() + running, s),
                      "compact");
             st.launches += (cr > 0 ? 1 : 0);
-            if (running) {
-                MCMI_TRY(launch_add_offset(rp_chunk, running, cr, s), "row_ptr offset");
+            if (running) {  // cr + 1: the chunk's end entry is the running total (row_ptr[rows] at the end)
+                MCMI_TRY(launch_add_offset(rp_chunk, running, cr + 1, s), "row_ptr offset");
                 st.launches += 1;
             }
         } else {
@@ -792,6 +812,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
                 MCMI_TRY(d2h(sink->values + running, vs, cn * sizeof(double)), "D2H val");
                 MCMI_TRY(cudaEventRecord(e->copy_done[c & 1], e->copy), "cudaEventRecord");
                 if (dbg) cudaEventRecord(dev[4 * c + 3], e->copy);
+                if (sink->queued) sink->queued(running, running + cn, e->copy);
                 st.launches += 2;
             }
         }
@@ -965,7 +986,11 @@ struct mcmi_result {
     }
 };
 
-// A host build running on a library thread (mcmi_build_start).
+// A host build running on a library thread (mcmi_build_start).  Once the
+// caller attaches its own entry arrays (mcmi_job_attach), a copier thread
+// moves every row chunk from the library's page-locked result into them as
+// soon as the chunk's device->host copy has completed, while later chunks are
+// still walking; mcmi_job_finish reports how many leading entries arrived.
 struct mcmi_job {
     mcmi_csr_view b{};
     mcmi_config cfg{};
@@ -978,6 +1003,71 @@ struct mcmi_job {
     int code = MCMI_OK;
     std::string msg;
     mcmi_result* result = nullptr;
+    // progressive delivery (guarded by mu)
+    struct Range {
+        int64_t lo, hi;
+        cudaEvent_t ev;
+    };
+    std::deque<Range> landed;       // queued chunk copies, in entry order
+    std::thread copier;
+    bool build_over = false;        // no more ranges will be queued
+    bool growing = false, busy = false;
+    int64_t* dst_col = nullptr;
+    double* dst_val = nullptr;
+    int64_t dst_cap = 0;
+    int64_t delivered = 0;          // entries [0, delivered) are in the attached arrays
+    const int64_t* src_col = nullptr;  // the result's current page-locked arrays
+    const double* src_val = nullptr;
+
+    void copier_loop() {
+        for (;;) {
+            Range rg{};
+            const int64_t* sc;
+            const double* sv;
+            int64_t* dc;
+            double* dv;
+            {
+                std::unique_lock<std::mutex> lk(mu);
+                cv.wait(lk, [&] {
+                    return (!landed.empty() && dst_col && !growing) || (build_over && (landed.empty() || !dst_col));
+                });
+                if (landed.empty() || !dst_col) return;  // the build thread destroys any events left
+                rg = landed.front();
+                landed.pop_front();
+                busy = true;
+                sc = src_col;
+                sv = src_val;
+                dc = dst_col;
+                dv = dst_val;
+            }
+            const bool ok = cudaEventSynchronize(rg.ev) == cudaSuccess;
+            cudaEventDestroy(rg.ev);
+            const int64_t hi_c = std::min(rg.hi, dst_cap);
+            bool advanced = false;
+            if (ok && rg.lo == delivered && hi_c > rg.lo) {  // ranges arrive in order
+                parallel_copy(dc + rg.lo, sc + rg.lo, static_cast<size_t>(hi_c - rg.lo) * sizeof(int64_t));
+                parallel_copy(dv + rg.lo, sv + rg.lo, static_cast<size_t>(hi_c - rg.lo) * sizeof(double));
+                advanced = true;
+            }
+            std::lock_guard<std::mutex> lk(mu);
+            if (advanced) delivered = hi_c;
+            busy = false;
+            cv.notify_all();
+        }
+    }
+    // the build thread is about to re-point the result's arrays: wait for the copier
+    void pause_copier() {
+        std::unique_lock<std::mutex> lk(mu);
+        growing = true;
+        cv.wait(lk, [&] { return !busy; });
+    }
+    void resume_copier(const int64_t* c, const double* v) {
+        std::lock_guard<std::mutex> lk(mu);
+        src_col = c;
+        src_val = v;
+        growing = false;
+        cv.notify_all();
+    }
 };
 
 namespace {
@@ -1171,7 +1261,7 @@ void free_parts(DeviceParts* r) {
 // then every GPU's shard copied to its global offset.
 Status build_host(const mcmi_csr_view& b, const mcmi_config& cfg, int64_t lo, int64_t hi, mcmi_result* r,
                   const std::function<void(int64_t)>& on_estimate, double first_chunk,
-                  const ApSource* ap_host = nullptr) {
+                  const ApSource* ap_host = nullptr, mcmi_job* job = nullptr) {
     std::vector<int> devs;
     if (Status st = shard_devices(cfg, &devs); st.code) return st;
     const int64_t n = b.n;
@@ -1219,13 +1309,14 @@ Status build_host(const mcmi_csr_view& b, const mcmi_config& cfg, int64_t lo, in
     sink.chains_used = r->cu.as<int64_t>();
     sink.entries_before = r->eb.as<int64_t>();
     sink.first_chunk = first_chunk;
-    sink.grow = [r](HostSink& sk, int64_t need_n, int64_t est, int64_t have) -> Status {
+    sink.grow = [r, job](HostSink& sk, int64_t need_n, int64_t est, int64_t have) -> Status {
         PinnedBuf nci = pinned_acquire(static_cast<size_t>(est) * 8), nv = pinned_acquire(static_cast<size_t>(est) * 8);
         if (!nci.p || !nv.p) {
             pinned_release(nci);
             pinned_release(nv);
             return fail(MCMI_ENOMEM, "cudaHostAlloc of " + std::to_string(need_n) + " result entries failed");
         }
+        if (job) job->pause_copier();
         if (have) {
             parallel_copy(nci.p, sk.col_idx, static_cast<size_t>(have) * 8);
             parallel_copy(nv.p, sk.values, static_cast<size_t>(have) * 8);
@@ -1237,8 +1328,23 @@ Status build_host(const mcmi_csr_view& b, const mcmi_config& cfg, int64_t lo, in
         sk.col_idx = nci.as<int64_t>();
         sk.values = nv.as<double>();
         sk.capacity = static_cast<int64_t>(std::min(nci.bytes, nv.bytes) / 8);
+        if (job) job->resume_copier(sk.col_idx, sk.values);
         return ok();
     };
+    if (job) {
+        sink.queued = [job](int64_t qlo, int64_t qhi, cudaStream_t copy) {
+            cudaEvent_t ev = nullptr;
+            if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess ||
+                cudaEventRecord(ev, copy) != cudaSuccess) {
+                cudaGetLastError();
+                if (ev) cudaEventDestroy(ev);
+                return;  // not delivered early: mcmi_job_finish reports the shorter prefix
+            }
+            std::lock_guard<std::mutex> lk(job->mu);
+            job->landed.push_back({qlo, qhi, ev});
+            job->cv.notify_all();
+        };
+    }
     bool published = false;
     sink.progress = [&](int64_t done, int64_t nnz_so_far, int64_t total) {
         if (published || !on_estimate) return;
@@ -1667,6 +1773,7 @@ int mcmi_build_start(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row
     j->lo = row_begin;
     j->hi = row_end;
     try {
+        j->copier = std::thread([j] { j->copier_loop(); });
         j->th = std::thread([j] {
             auto* r = new mcmi_result();
             auto publish = [j](int64_t est) {
@@ -1679,8 +1786,16 @@ int mcmi_build_start(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row
             };
             // a small first chunk (10% of the rows) gives the caller its entry
             // estimate early enough to size its own arrays while the walks run
-            const Status st = build_host(j->b, j->cfg, j->lo, j->hi, r, publish, 0.1);
+            const Status st = build_host(j->b, j->cfg, j->lo, j->hi, r, publish, 0.1, nullptr, j);
+            {
+                std::lock_guard<std::mutex> lk(j->mu);
+                j->build_over = true;
+                j->cv.notify_all();
+            }
+            if (j->copier.joinable()) j->copier.join();
             std::lock_guard<std::mutex> lk(j->mu);
+            for (auto& rg : j->landed) cudaEventDestroy(rg.ev);
+            j->landed.clear();
             if (st.code) {
                 delete r;
                 r = nullptr;
@@ -1695,6 +1810,14 @@ int mcmi_build_start(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row
             j->cv.notify_all();
         });
     } catch (const std::exception& ex) {
+        if (j->copier.joinable()) {
+            {
+                std::lock_guard<std::mutex> lk(j->mu);
+                j->build_over = true;
+                j->cv.notify_all();
+            }
+            j->copier.join();
+        }
         delete j;
         return report(fail(MCMI_ENOMEM, std::string("cannot start the build thread: ") + ex.what()), err, errlen);
     }
@@ -1710,9 +1833,23 @@ int mcmi_job_estimate(mcmi_job* job, int64_t* nnz_estimate) {
     return job->done ? job->code : MCMI_OK;
 }
 
-int mcmi_job_finish(mcmi_job* job, mcmi_result** out, char* err, size_t errlen) {
+int mcmi_job_attach(mcmi_job* job, int64_t* col_idx, double* values, int64_t capacity) {
+    if (!job || (capacity > 0 && (!col_idx || !values))) return MCMI_EINVAL;
+    std::lock_guard<std::mutex> lk(job->mu);
+    if (job->dst_col) return MCMI_EINVAL;  // once per job
+    if (capacity <= 0) return MCMI_OK;
+    job->dst_col = col_idx;
+    job->dst_val = values;
+    job->dst_cap = capacity;
+    job->cv.notify_all();
+    return MCMI_OK;
+}
+
+int mcmi_job_finish(mcmi_job* job, mcmi_result** out, int64_t* delivered, char* err, size_t errlen) {
+    if (delivered) *delivered = 0;
     if (!job) return report(fail(MCMI_EINVAL, "null argument"), err, errlen);
     if (job->th.joinable()) job->th.join();
+    if (delivered && job->result) *delivered = std::min(job->delivered, job->result->nnz);
     const Status st{job->code, job->msg};
     if (out) {
         *out = job->result;
@@ -1916,6 +2053,15 @@ int mcmi_result_copy(const mcmi_result* r, int64_t* row_ptr, int64_t* col_idx, d
     cp(entries_before, r->eb, r->n);
     if (n_chains) *n_chains = r->n_chains;
     if (max_len) *max_len = r->max_len;
+    return MCMI_OK;
+}
+
+int mcmi_result_copy_range(const mcmi_result* r, int64_t begin, int64_t end, int64_t* col_idx, double* values) {
+    if (!r || begin < 0 || end < begin || end > r->nnz) return MCMI_EINVAL;
+    if (end == begin) return MCMI_OK;
+    const size_t bytes = static_cast<size_t>(end - begin) * 8;
+    if (col_idx) parallel_copy(col_idx + begin, r->ci.as<int64_t>() + begin, bytes);
+    if (values) parallel_copy(values + begin, r->v.as<double>() + begin, bytes);
     return MCMI_OK;
 }
 

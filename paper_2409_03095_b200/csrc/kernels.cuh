@@ -43,13 +43,17 @@ struct Reductions {
 
 // Transition tables (subsystem 1), one 32-byte record per state s:
 //   rec[2s]   = {begin, deg, guide[0..3], guide[4..7]}
-//   rec[2s+1] = {guide[8..11], guide[12..15], col (deg==1), 0}
+//   rec[2s+1] = {guide[8..11], guide[12..15], col (deg==1), guide scale ceil(deg/255)}
 //   deg == 1 : rec[2s].zw holds the forced move's ratio (f64) instead of guide[0..7]
 //   guide[m] (u8, in units of ceil(deg/255)) = first k with cum_k > m/16, so the
 //   inverse-CDF scan for u starts at guide[floor(16u)] and returns the same k as
 //   the reference's full scan (all skipped cum_k <= m/16 <= u).
 //   ent[k]  = {cum_k, ratio_k}: running sequential sum of p (sample_transition's
-//             `cum`, mc_engine.cpp:71-75) and a_k / p_k (mc_engine.cpp:94)
+//             `cum`, mc_engine.cpp:71-75) and a_k / p_k (mc_engine.cpp:94); the
+//             last entry of a row with deg >= 2 stores cum = +inf, which makes
+//             "first k with u < cum_k" return end-1 exactly when the reference's
+//             scan falls through to its end-1 fallback (mc_engine.cpp:76), so the
+//             device scan needs no bound or fallback
 //   col[k]  = column of A (int32)
 constexpr int kGuide = 16;
 
@@ -59,6 +63,7 @@ struct Tables {
     const double2* ent;
     const int* col;
     const double* b1_diag;  // diag(B_hat) = B1 (split.cpp:70)
+    const unsigned char* tri;  // [n] L = 2 split-fold rows (k_tri_free), or nullptr
 };
 
 struct TableBuildArgs {
@@ -127,9 +132,11 @@ struct WalkArgs {
     const int* row_list;    // nullptr: work item i is row row_begin + work_offset + i
     int64_t work_offset;
     int64_t n_work;
+    int claim_rows;         // consecutive work items a warp claims at once (1 for row lists)
     int64_t n_chains, max_len;
     double delta;
     uint64_t seed;
+    uint32_t rk[20];        // Philox round keys of `seed` (launch_walk fills them)
     int64_t retain_k;
     int rng_mode;
     int cap;                // hash capacity (power of two)
@@ -165,6 +172,7 @@ cudaError_t launch_table_build(const TableBuildArgs& a, int64_t nnz, bool drop_a
                                cudaStream_t s);
 cudaError_t launch_table_fill(const TableBuildArgs& a, cudaStream_t s);
 cudaError_t launch_ap_tables(const ApTableArgs& a, cudaStream_t s);
+cudaError_t launch_tri_free(const uint4* rec, const int* col, int64_t n, unsigned char* tri, cudaStream_t s);
 // drop_small_entries: pass 0 row counts (value range first), pass 1 fill.
 cudaError_t launch_drop_filter(const TableBuildArgs& a, bool drop_active, int pass, int* cnt, const int64_t* out_rp,
                                int64_t* oci, double* ov, cudaStream_t s);

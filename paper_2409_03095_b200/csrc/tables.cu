@@ -278,6 +278,7 @@ __global__ void k_rows_fill(TableBuildArgs a) {
                 const double p = fabs(av) / row_sum;
                 cum += p;
                 const double ratio = av / p;
+                if (o + 1 == cnt && cnt >= 2) cum = __longlong_as_double(0x7ff0000000000000ll);  // +inf: the fallback
                 a.ent[begin + o] = make_double2(cum, ratio);
                 a.col[begin + o] = static_cast<int>(c);
                 if (cnt == 1) {
@@ -301,6 +302,7 @@ __global__ void k_rows_fill(TableBuildArgs a) {
                 r0.w = w[1];
                 r1.x = w[2];
                 r1.y = w[3];
+                r1.w = scale;
             }
         }
         a.rec[2 * i] = r0;
@@ -331,6 +333,7 @@ __global__ void k_ap_fill(ApTableArgs a) {
             cum += p;  // sample_transition's running sum (mc_engine.cpp:71-75)
             const double ratio = a.a_values[k] / p;  // mc_engine.cpp:94
             const unsigned o = static_cast<unsigned>(k - k0);
+            if (o + 1 == cnt && cnt >= 2) cum = __longlong_as_double(0x7ff0000000000000ll);  // +inf: the fallback
             a.ent[k] = make_double2(cum, ratio);
             a.col[k] = static_cast<int>(c);
             if (cnt == 1) {
@@ -352,6 +355,7 @@ __global__ void k_ap_fill(ApTableArgs a) {
             r0.w = w[1];
             r1.x = w[2];
             r1.y = w[3];
+            r1.w = scale;
         }
         a.rec[2 * i] = r0;
         a.rec[2 * i + 1] = r1;
@@ -364,6 +368,38 @@ __global__ void k_ap_fill(ApTableArgs a) {
     if (threadIdx.x == 0) {
         atomicMax(&a.red->max_deg, md);
         atomicAdd(&a.red->a_nnz, nnz_a);
+    }
+}
+
+// Rows whose L = 2 walks can use the split fold of walk.cu: r has at most
+// kTriDeg transitions, each neighbour j has at most kTriNbDeg, and no neighbour
+// of a neighbour is itself a neighbour of r (no triangle through r; A has no
+// self loops).  Then a step-0 deposit only ever lands on a neighbour c_k with
+// the fixed value ratio_k, and no step-1 deposit lands there.  O(deg^2 * deg_j)
+// per row, run only for L = 2 builds.
+constexpr unsigned kTriDeg = 16, kTriNbDeg = 64;
+__global__ void k_tri_free(const uint4* __restrict__ rec, const int* __restrict__ col, int64_t n,
+                           unsigned char* __restrict__ tri) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const uint4 r0 = rec[2 * i];
+        const unsigned b = r0.x, d = r0.y;
+        bool tf = d >= 1 && d <= kTriDeg;
+        for (unsigned a = 0; tf && a < d; ++a) {
+            const uint4 q = rec[2 * static_cast<int64_t>(col[b + a])];
+            if (q.y > kTriNbDeg) {
+                tf = false;
+                break;
+            }
+            for (unsigned x = 0; tf && x < q.y; ++x) {
+                const int c = col[q.x + x];
+                for (unsigned e = 0; e < d; ++e)
+                    if (col[b + e] == c) {
+                        tf = false;
+                        break;
+                    }
+            }
+        }
+        tri[i] = tf ? 1 : 0;
     }
 }
 
@@ -669,6 +705,11 @@ cudaError_t launch_table_build(const TableBuildArgs& a, int64_t /*nnz*/, bool dr
     if (drop_active && a.drop_mode == 0) k_offdiag_range<<<g, TB, 0, s>>>(a);
     k_rows_norm<<<g, TB, 0, s>>>(a);
     k_rows_split<<<g, TB, 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_tri_free(const uint4* rec, const int* col, int64_t n, unsigned char* tri, cudaStream_t s) {
+    if (n > 0) k_tri_free<<<grid_for(n), TB, 0, s>>>(rec, col, n, tri);
     return cudaGetLastError();
 }
 

@@ -140,11 +140,9 @@ __device__ __forceinline__ int hash_slot(int* keys, unsigned mask, int shift, in
 // an exactly representable multiple of ulp(acc), so those additions collapse
 // into one exact addition; the addition that crosses 2^(e+1) is performed on
 // its own (it may round).  A run therefore costs O(binade crossings), not O(k).
-__device__ __forceinline__ double add_ones(double acc, int k) {
-    if (acc >= 1.0 && acc < 0x1.0p53) {  // common case: no binade crossing
-        const double t = acc + static_cast<double>(k);
-        if ((__double_as_longlong(t) >> 52) == (__double_as_longlong(acc) >> 52)) return t;
-    }
+__device__ __forceinline__ double add_ones_slow(double acc, int k) {
+    // an integer-valued acc (no return weight added yet) stays exact
+    if (acc == floor(acc) && fabs(acc) + static_cast<double>(k) < 0x1.0p53) return acc + static_cast<double>(k);
     while (k > 0) {
         if (!(acc >= 1.0 && acc < 0x1.0p53)) {  // acc == 0 (row start) or out of range
             acc += 1.0;
@@ -167,6 +165,24 @@ __device__ __forceinline__ double add_ones(double acc, int k) {
         }
     }
     return acc;
+}
+
+// The same in one addition whenever 1 <= acc < 2^50 and
+// acc + k stays below 2^(e+2) (at most one binade crossing).  Proof: with
+// u = ulp(acc), the k sequential additions are exact until the one that
+// crosses 2^(e+1); that one rounds X + 1 to the 2u grid (ties to even), and
+// the remaining m additions are exact again.  A single rounding of acc + k =
+// (X + 1) + m gives the same value because m is a multiple of 2u that is an
+// EVEN multiple (m * 2^(51-e), e <= 50), so shifting by m preserves both the
+// nearest 2u-grid point and, for a tie, its parity.  Everything else (acc < 1,
+// two crossings, acc >= 2^50) takes the exact loop.
+__device__ __forceinline__ double add_ones(double acc, int k) {
+    const int hi = __double2hiint(acc);
+    const double top2 = __hiloint2double((hi & 0x7ff00000) + 0x00200000, 0);  // 2^(e+2)
+    const double t = acc + static_cast<double>(k);
+    // 1 <= acc < 2^50 (sign bit clear): one unsigned range test on the high word
+    if (static_cast<unsigned>(hi - 0x3ff00000) < 0x03200000u && t < top2) return t;
+    return add_ones_slow(acc, k);
 }
 
 // Keeps the lowest `keep` set bits of mask (keep >= 0).
@@ -437,6 +453,20 @@ constexpr int kNbDeg = 32;    // max deg(r)
 constexpr int kNbT2 = 704;    // max sum of the neighbours' degrees
 constexpr int kNbBytes = 32 + 2 * kNbDeg + kNbDeg + kNbT2;  // mask[8] u32, off[32] u16, T1[32] u8, T2 u8
 
+// Split fold (L = 2 kernels without NB tables, rows flagged by k_tri_free):
+// no triangle through r, so a step-0 deposit lands only on a neighbour c_k of
+// r, always with the value ratio_k = a/p of transition k (mc_engine.cpp:94),
+// and no step-1 deposit lands there.  Column c_k's ordered sum is therefore
+// m_k sequential additions of ratio_k, m_k = the chains whose first step took
+// transition k: the batches only count them (per-warp counters), the fold of
+// the log covers the step-1 deposits alone (one 32-entry chunk per batch
+// instead of two), and c_k's sums are formed once per row.  Bit-identical.
+constexpr int kTfBytes = 32 * 4;  // per-warp m_k counters (deg(r) <= 16)
+template <int LF, bool NB>
+__host__ __device__ constexpr bool split_fold_kernel() {
+    return LF == 2 && !NB;
+}
+
 template <int MODE, int MINB, bool GL, bool DEG, int LF = 0, int CAPC = 0, bool NB = false>
 __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     static_assert(!NB || (LF == 2 && CAPC >= 32 && CAPC <= 256 && !GL), "NB: L = 2 kernel, shared tiers");
@@ -454,8 +484,10 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     const int S = LF ? LF : a.log_stride;       // step deposits per chain (max_len)
     const int B = LF ? 32 : a.lanes;            // chains per batch
     const int logn = LF ? round32(32 * LF) : a.log_n;  // round32(B * S), host-computed (kernel parameter)
-    const size_t per_warp = (LF && CAPC) ? static_cast<size_t>(CAPC + logn) * 12 + (NB ? kNbBytes : 0)
-                                         : static_cast<size_t>(a.warp_bytes);
+    constexpr bool kTF = split_fold_kernel<LF, NB>();
+    const size_t per_warp = (LF && CAPC) ? static_cast<size_t>(CAPC + logn) * 12 + (NB ? kNbBytes : 0) +
+                                               (kTF ? kTfBytes : 0)
+                                         : static_cast<size_t>(a.warp_bytes) + (kTF ? kTfBytes : 0);
     // GL: per-warp accumulator + log in global scratch (large rows / long walks)
     unsigned char* wbase = GL ? a.gscratch + per_warp * (static_cast<size_t>(blockIdx.x) * (blockDim.x >> 5) + warp)
                               : smem_raw + per_warp * warp;
@@ -465,6 +497,8 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     unsigned short* const nb_off = NB ? reinterpret_cast<unsigned short*>(nb_mask + 8) : nullptr;
     unsigned char* const nb_t1 = NB ? reinterpret_cast<unsigned char*>(nb_off + kNbDeg) : nullptr;
     unsigned char* const nb_t2 = NB ? nb_t1 + kNbDeg : nullptr;
+    // split-fold counters m_k after the log (per_warp - kTfBytes)
+    int* const tf_cnt = kTF ? reinterpret_cast<int*>(wbase + (per_warp - kTfBytes)) : nullptr;
     const unsigned cap_mask = static_cast<unsigned>(cap - 1);
     const int shift = CAPC ? 32 - (31 - __clz(CAPC)) : a.hash_shift;  // 32 - log2(cap)
     const unsigned lt_mask = (1u << lane) - 1u;
@@ -473,7 +507,6 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     const uint4* __restrict__ rec = a.t.rec;
     const double2* __restrict__ ent = a.t.ent;
     const int* __restrict__ tcol = a.t.col;
-    const uint2 key = make_uint2(static_cast<uint32_t>(a.seed), static_cast<uint32_t>(a.seed >> 32));
     // host guarantees 1 <= N < 2^31 and L < 2^31 (engine.cu), so 32-bit loop state
     const int N = static_cast<int>(a.n_chains);
     const int L = LF ? LF : static_cast<int>(a.max_len);
@@ -487,11 +520,26 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     }
     __syncwarp();
 
+    // Rows are claimed R = claim_rows consecutive work items at a time (a warp
+    // walks neighbouring rows back to back, so their shared 2-hop records are
+    // still in its SM's L1), one claim ahead, so the cursor atomic's round trip
+    // overlaps the current rows' walks.
+    const int R = a.claim_rows;
+    int claimed = 0;
+    if (lane == 0) claimed = static_cast<int>(atomicAdd(&a.counters[0], static_cast<unsigned long long>(R)));
+    int cur = 0, cur_end = 0;
     for (;;) {
-        int wi = 0;
-        if (lane == 0) wi = static_cast<int>(atomicAdd(&a.counters[0], 1ull));
-        wi = __shfl_sync(FULL_MASK, wi, 0);
-        if (wi >= a.n_work) break;
+        if (cur >= cur_end) {
+            cur = __shfl_sync(FULL_MASK, claimed, 0);
+            cur_end = cur + R;
+            if (cur >= a.n_work) break;
+            if (lane == 0) claimed = static_cast<int>(atomicAdd(&a.counters[0], static_cast<unsigned long long>(R)));
+        }
+        const int wi = cur++;
+        if (wi >= a.n_work) {
+            cur = cur_end;
+            continue;
+        }
         const int row = a.row_list ? a.row_list[wi] : static_cast<int>(a.row_begin + a.work_offset) + wi;
         const int rowc = static_cast<int>(row);
 
@@ -561,6 +609,12 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             __syncwarp();
         }
         const int rkey = (NB && nb) ? slot_r : rowc;  // log key of column r
+        // split fold for this row (warp-uniform)
+        const bool tf = kTF && a.t.tri != nullptr && a.t.tri[rowc] != 0;
+        if (kTF && tf) {
+            tf_cnt[lane] = 0;
+            __syncwarp();
+        }
 
         int distinct = 1;
         bool overflow = false;
@@ -601,6 +655,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             bool alive = active;
             bool log_full = false;  // the walk would outgrow this tier's deposit log
             unsigned nb_i1 = 0;     // NB: entry index of the first step in row r
+            int k1 = 0;             // split fold: transition index of the first step
 #pragma unroll
             for (int t = 0; LF ? (t < LF) : __any_sync(FULL_MASK, alive); ++t) {
                 if (LF) {  // compile-time trip count: no log overflow, no length test
@@ -629,63 +684,60 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                     ratio = __hiloint2double(static_cast<int>(r0.w), static_cast<int>(r0.z));
                     nxt = static_cast<int>(r1.z);
                 } else {
-                    double u;
+                    uint32_t ulo, uhi;  // the draw's two words, lo first (rng.hpp:32-41)
                     if (IS_REF) {
                         const PosT b = pos >> 1;
                         if (b != cached) {
-                            blk = philox4x32_10(
+                            blk = philox4x32_10_rk(
                                 make_uint4(static_cast<uint32_t>(b),
                                            static_cast<uint32_t>(static_cast<unsigned long long>(b) >> 32),
                                            static_cast<uint32_t>(row),
                                            0u),  // row < 2^31: stream id high word
-                                key);
+                                a.rk);
                             cached = b;
                         }
-                        u = (pos & 1) ? u32pair_to_double(blk.z, blk.w)
-                                      : u32pair_to_double(blk.x, blk.y);
+                        ulo = (pos & 1) ? blk.z : blk.x;
+                        uhi = (pos & 1) ? blk.w : blk.y;
                         ++pos;
                     } else {
                         const PosT b = static_cast<unsigned>(t) >> 1;
                         if (b != cached) {
-                            blk = philox4x32_10(
+                            blk = philox4x32_10_rk(
                                 make_uint4(static_cast<uint32_t>(b), static_cast<uint32_t>(chain),
                                            static_cast<uint32_t>(row),
                                            0u),  // row < 2^31: stream id high word
-                                key);
+                                a.rk);
                             cached = b;
                         }
-                        u = (t & 1) ? u32pair_to_double(blk.z, blk.w)
-                                    : u32pair_to_double(blk.x, blk.y);
+                        ulo = (t & 1) ? blk.z : blk.x;
+                        uhi = (t & 1) ? blk.w : blk.y;
                     }
+                    const double u = u32pair_to_double(ulo, uhi);
                     ++draws;
-                    // inverse CDF (mc_engine.cpp:71-77): first k with u < cum_k, else
-                    // the last entry.  Start at the guide bucket of u: every skipped
-                    // entry has cum <= m/16 <= u.
-                    const int mb = static_cast<int>(u * static_cast<double>(kGuide));
+                    // inverse CDF (mc_engine.cpp:71-77): first k with u < cum_k; the
+                    // row's last cum is +inf in the table, which is the reference's
+                    // end-1 fallback.  Start at the guide bucket of u, floor(16 u) =
+                    // the top 4 bits of the 53-bit draw: every skipped entry has
+                    // cum <= m/16 <= u.
+                    const unsigned mb = uhi >> 28;
                     const unsigned gw = mb < 8 ? (mb < 4 ? r0.z : r0.w) : (mb < 12 ? r1.x : r1.y);
                     const unsigned g = (gw >> ((mb & 3) * 8)) & 0xffu;
-                    const unsigned end = r0.x + deg;
-                    unsigned q = r0.x + g * ((deg + 254u) / 255u);
-                    unsigned k = end - 1;
-                    bool found = false;
-                    ratio = 0.0;
-                    for (; q < end; q += 2) {
+                    unsigned q = r0.x + g * r1.w;  // r1.w = guide scale ceil(deg / 255)
+                    unsigned k;
+                    for (;; q += 2) {
                         const double2 e0 = ent[q];
-                        const double2 e1 = ent[min(q + 1, end - 1)];
+                        const double2 e1 = ent[q + 1];  // past the row only when e0 is its +inf entry
                         if (u < e0.x) {
                             k = q;
                             ratio = e0.y;
-                            found = true;
                             break;
                         }
                         if (u < e1.x) {
-                            k = min(q + 1, end - 1);
+                            k = q + 1;
                             ratio = e1.y;
-                            found = true;
                             break;
                         }
                     }
-                    if (!found) ratio = ent[end - 1].y;
                     kidx = k - r0.x;
                     if (!(NB && nb && t == 1)) nxt = tcol[k];  // NB: the last step logs a slot only
                 }
@@ -703,12 +755,20 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                     state = nxt;
                     logv = state;
                 }
-                lc[m * B] = logv;
-                lw[m * B] = w;
+                // a lane writes deposit m at step t with m == t (alive lanes never
+                // skip a step), so LF kernels index the log with the compile-time t
+                const int mi = LF ? t : m;
+                if (kTF && tf && t == 0) {
+                    k1 = static_cast<int>(kidx);  // counted, not logged (split fold)
+                } else {
+                    lc[mi * B] = logv;
+                    lw[mi * B] = w;
+                }
                 ++m;
                 if (logv == rkey) {
                     if (retm == 0 && !ret_hi) ret_w = w;
-                    if (m <= 32) retm |= 1u << (m - 1);
+                    if (LF && LF <= 32) retm |= 1u << t;
+                    else if (m <= 32) retm |= 1u << (m - 1);
                     else ret_hi = true;
                 }
                 if (fabs(w) < a.delta) alive = false;  // mc_engine.cpp:97
@@ -781,6 +841,13 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             }
             __syncwarp();
 
+            // split fold: count this batch's first steps per transition of r
+            if (kTF && tf) {
+                const bool took0 = mine && m >= 1;
+                const unsigned pk = __match_any_sync(FULL_MASK, took0 ? k1 : -1 - lane);
+                if (took0 && (pk & lt_mask) == 0) tf_cnt[k1] += __popc(pk);
+                __syncwarp();
+            }
             // ------------------------------------- ordered (chain, step) fold
             // (i) column r: W0 = +1.0 per valid chain plus its returns, in
             // chain order, folded in a register (warp-uniform).
@@ -789,7 +856,11 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 if (rl == 0) {
                     acc_r = add_ones(acc_r, __popc(valid));
                 } else {
-                    const unsigned multi = __ballot_sync(FULL_MASK, mine && ((retm & (retm - 1)) != 0 || ret_hi));
+                    // L <= 2: a chain returns to r at most once (A has no self loops,
+                    // so only its last step can land on r)
+                    constexpr bool kMulti = LF == 0 || LF > 2;
+                    const unsigned multi =
+                        kMulti ? __ballot_sync(FULL_MASK, mine && ((retm & (retm - 1)) != 0 || ret_hi)) : 0u;
                     // W0 additions owed before this lane's return: valid chains after
                     // the previous returning lane, up to and including this one
                     const unsigned prevs = rl & lt_mask;
@@ -801,7 +872,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                         todo &= todo - 1;
                         acc_r = add_ones(acc_r, __shfl_sync(FULL_MASK, run, j));
                         acc_r += __shfl_sync(FULL_MASK, ret_w, j);  // first return of chain j
-                        if ((multi >> j) & 1u) {  // later returns of chain j, in step order
+                        if (kMulti && ((multi >> j) & 1u)) {  // later returns of chain j, in step order
                             const unsigned rm = __shfl_sync(FULL_MASK, retm, j);
                             const bool hi = __shfl_sync(FULL_MASK, static_cast<int>(ret_hi), j) != 0;
                             unsigned rest = rm & (rm - 1);
@@ -831,15 +902,19 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             // as a shuffle chain in lane (= chain-major) order.
             int n_new = 0;
             bool fail = false;
-            const int span = B * S;
+            // split fold: only the step-1 deposits (position p = chain j, step 1)
+            const int span = (kTF && tf) ? B : B * S;
             for (int base = 0; base < span; base += 32) {
                 const int p = base + lane;
                 // chain of position p: p / S (shift for power-of-two S, else the magic multiply)
-                const int j = min(s_shift >= 0 ? (p >> s_shift)
-                                               : static_cast<int>(__umulhi(static_cast<unsigned>(p), a.log_magic)),
-                                  31);
+                const int j = (kTF && tf) ? p
+                                          : min(s_shift >= 0 ? (p >> s_shift)
+                                                             : static_cast<int>(
+                                                                   __umulhi(static_cast<unsigned>(p), a.log_magic)),
+                                                31);
                 bool ok = p < span && ((valid >> j) & 1u);
-                const int q = (p - j * S) * B + j;  // chain-major position p -> step-major slot
+                // chain-major position p -> step-major slot
+                const int q = (kTF && tf) ? B + j : (p - j * S) * B + j;
                 int c = ok ? sm.log_col[q] : -1;
                 ok = ok && c >= 0 && c != rkey;  // column r was folded in (i)
                 if (!ok) c = -1 - lane;          // unique non-column tag
@@ -884,6 +959,29 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             if (chains_done >= N) row_done = true;
         }
 
+        if (kTF && tf && !overflow) {
+            // split fold: column c_k = m_k sequential additions of ratio_k, in
+            // chain order (all equal, so only the count matters); c_k was never
+            // touched by a step-1 deposit, so this inserts it
+            uint4 q0, q1;
+            ldg256(rec + 2 * static_cast<int64_t>(rowc), q0, q1);
+            int nn = 0;
+            bool bad = false;
+            if (static_cast<unsigned>(lane) < q0.y) {
+                const int mk = tf_cnt[lane];
+                if (mk > 0) {
+                    const double rk = ent[q0.x + lane].y;
+                    double v = 0.0;
+                    for (int i = 0; i < mk; ++i) v += rk;  // mc_engine.cpp:49, chain order
+                    const int sl = hash_slot<GL>(sm.keys, cap_mask, shift, tcol[q0.x + lane], nn);
+                    if (sl < 0) bad = true;
+                    else sm.vals[sl] = v;
+                }
+            }
+            distinct += warp_sum_int(nn);
+            if (__any_sync(FULL_MASK, bad) || distinct > (CAPC ? CAPC - CAPC / 4 : a.cap_limit)) overflow = true;
+            __syncwarp();
+        }
         const int64_t lrow = static_cast<int64_t>(row) - a.row_begin;
         if (overflow) {
             if (lane == 0) {
@@ -1047,7 +1145,10 @@ template <int MODE, int MINB, bool GL, bool DEG, int LF = 0, int CAPC = 0, bool 
 cudaError_t launch_walk_t(const WalkArgs& a, int warps_per_block, int num_sms, int64_t max_warps,
                           cudaStream_t s) {
     const size_t smem =
-        GL ? 0 : (walk_smem_bytes_per_warp(a.cap, a.lanes, a.log_stride) + (NB ? kNbBytes : 0)) * warps_per_block;
+        GL ? 0
+           : (walk_smem_bytes_per_warp(a.cap, a.lanes, a.log_stride) + (NB ? kNbBytes : 0) +
+              (split_fold_kernel<LF, NB>() ? kTfBytes : 0)) *
+                 warps_per_block;
     const int threads = warps_per_block * 32;
     cudaError_t e = cudaFuncSetAttribute(k_walk<MODE, MINB, GL, DEG, LF, CAPC, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          static_cast<int>(smem));
@@ -1124,6 +1225,13 @@ cudaError_t launch_walk(const WalkArgs& a_in, int warps_per_block, int num_sms, 
                         int64_t max_warps, cudaStream_t s) {
     if (a_in.n_work <= 0) return cudaSuccess;
     WalkArgs a = a_in;  // derived per-launch constants, so the kernel re-reads rather than recomputes them
+    {  // Philox round keys of the master seed (rng.hpp:56-66 key schedule)
+        uint32_t k0 = static_cast<uint32_t>(a.seed), k1 = static_cast<uint32_t>(a.seed >> 32);
+        for (int r = 0; r < 10; ++r, k0 += 0x9E3779B9u, k1 += 0xBB67AE85u) {
+            a.rk[2 * r] = k0;
+            a.rk[2 * r + 1] = k1;
+        }
+    }
     a.log_n = round32(a.lanes * a.log_stride);
     a.warp_bytes = static_cast<long long>(walk_smem_bytes_per_warp(a.cap, a.lanes, a.log_stride));
     {

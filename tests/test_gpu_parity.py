@@ -468,3 +468,93 @@ def test_neighbourhood_slot_tables_match_plain_kernel(mc, oracle_mod, rng, over,
         a, z = nbk.m.row_ptr[lo], nbk.m.row_ptr[hi]
         assert np.array_equal(nbk.m.col_idx[a:z], want.col_idx) and bits_equal(nbk.m.values[a:z], want.values)
         assert np.array_equal(nbk.row_meta.entries_before_retention[lo:hi], want.entries_before)
+
+
+def _mixed_triangle_matrix(mc, n=400, seed=3):
+    """Rows with and without triangles through them: a ring (triangle-free)
+    plus random chords, some closing triangles; degrees 2..8."""
+    rng = np.random.default_rng(seed)
+    rows, cols, vals = [], [], []
+    for i in range(n):
+        nb = {(i + 1) % n, (i - 1) % n}
+        if rng.random() < 0.5:
+            nb |= set(int(x) for x in rng.integers(0, n, size=int(rng.integers(1, 6))))
+        if rng.random() < 0.3:
+            nb.add((i + 2) % n)  # with i+1 -> i+2 a triangle through i
+        nb.discard(i)
+        for c in nb:
+            rows.append(i)
+            cols.append(c)
+            vals.append(-rng.uniform(0.2, 1.0))
+        rows.append(i)
+        cols.append(i)
+        vals.append(10.0)
+    return mc.CsrMatrix.from_triplets(n, rows, cols, vals)
+
+
+@pytest.mark.parametrize("rng", [0, 1])
+@pytest.mark.parametrize("over", [{}, {"chains_override": 77, "max_len_override": 2, "delta": 0.2},
+                                  {"retain_k": 4, "master_seed": 9}, {"epsilon": 0.02, "delta": 0.01}])
+@pytest.mark.parametrize("gen", ["laplacian3d", "convdiff", "mixed"])
+def test_split_fold_matches_plain_kernel(mc, oracle_mod, rng, over, gen, monkeypatch):
+    """The L = 2 split fold (rows without a triangle through r: step-0 columns
+    summed from per-transition counts) equals the plain ordered fold
+    (MCMI_WALK_NO_SPLIT=1) bit for bit, RowMeta included, and the oracle."""
+    from paper_2409_03095_b200 import generators as G
+    b = {"laplacian3d": lambda: G.laplacian3d(12), "convdiff": lambda: G.convection_diffusion(30),
+         "mixed": lambda: _mixed_triangle_matrix(mc)}[gen]()
+    cfg = mc.McConfig(rng_mode=rng, **over)
+    split = mc.compute_preconditioner(b, cfg)
+    assert split.budget_echo.max_len == 2
+    monkeypatch.setenv("MCMI_WALK_NO_SPLIT", "1")
+    plain = mc.compute_preconditioner(b, cfg)
+    monkeypatch.delenv("MCMI_WALK_NO_SPLIT")
+    assert split.m == plain.m and split.stats["walk_steps"] == plain.stats["walk_steps"]
+    assert np.array_equal(split.row_meta.entries_before_retention, plain.row_meta.entries_before_retention)
+    assert np.array_equal(split.row_meta.chains_used, plain.row_meta.chains_used)
+    want = oracle_mod.compute_preconditioner(b.n, b.row_ptr, b.col_idx, b.values, **cfg.oracle_kwargs())
+    assert np.array_equal(split.m.row_ptr, want.row_ptr) and np.array_equal(split.m.col_idx, want.col_idx)
+    assert bits_equal(split.m.values, want.values)
+
+
+@pytest.mark.parametrize("cap_mode", ["estimate", "short", "none"])
+def test_job_api_progressive_delivery(mc, cap_mode):
+    """mcmi_build_start / mcmi_job_estimate / mcmi_job_attach / mcmi_job_finish /
+    mcmi_result_copy_range (the C++ drop-in's path): chunks delivered into the
+    caller's arrays during the build plus the copied tail equal the handle
+    path, for an attach at the estimate, a too-short attach and none."""
+    import ctypes as C
+    from paper_2409_03095_b200 import _lib as L
+    from paper_2409_03095_b200 import generators as G
+    lib = L.load()
+    b = G.laplacian3d(64)  # 262,144 rows: 4 streamed chunks, first at 10%
+    cfg = mc.McConfig(master_seed=5)
+    want = mc.compute_preconditioner(b, cfg)
+    view = L.mcmi_csr_view(b.n, b.row_ptr.ctypes.data, b.col_idx.ctypes.data, b.values.ctypes.data)
+    c = cfg.to_c()
+    job = C.c_void_p()
+    err = C.create_string_buffer(512)
+    assert lib.mcmi_build_start(C.byref(view), C.byref(c), 0, -1, C.byref(job), err, 512) == 0
+    est = C.c_int64()
+    assert lib.mcmi_job_estimate(job, C.byref(est)) == 0
+    nnz = want.m.nnz()
+    assert est.value >= nnz * 0.9  # upper-biased extrapolation of the first chunk
+    cap = {"estimate": est.value, "short": nnz // 3, "none": 0}[cap_mode]
+    col = np.full(max(cap, nnz), -7, np.int64)
+    val = np.full(max(cap, nnz), np.nan)
+    if cap:
+        assert lib.mcmi_job_attach(job, col.ctypes.data, val.ctypes.data, cap) == 0
+    res = C.c_void_p()
+    delivered = C.c_int64()
+    assert lib.mcmi_job_finish(job, C.byref(res), C.byref(delivered), err, 512) == 0
+    try:
+        got_n, got_nnz = C.c_int64(), C.c_int64()
+        lib.mcmi_result_sizes(res, C.byref(got_n), C.byref(got_nnz))
+        assert got_nnz.value == nnz and 0 <= delivered.value <= min(cap, nnz)
+        if cap_mode == "none":
+            assert delivered.value == 0
+        assert lib.mcmi_result_copy_range(res, delivered.value, nnz, col.ctypes.data, val.ctypes.data) == 0
+        assert np.array_equal(col[:nnz], want.m.col_idx) and bits_equal(val[:nnz], want.m.values)
+        assert lib.mcmi_result_copy_range(res, 5, 3, None, None) == L.MCMI_EINVAL
+    finally:
+        lib.mcmi_result_free(res)

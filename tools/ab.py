@@ -28,8 +28,8 @@ def build(name, src=None, defines=()):
     out = os.path.join(HERE, "_build", name, "libmcmi.so")
     os.makedirs(os.path.dirname(out), exist_ok=True)
     nvcc = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
-    cmd = [nvcc, *B.NVCC_FLAGS, *[f"-D{d}" for d in defines], "-o", out]
-    cmd += [os.path.join(src, f) for f in B.SOURCES]
+    cmd = [nvcc, *B.NVCC_FLAGS, "-shared", *[f"-D{d}" for d in defines], "-o", out]
+    cmd += [os.path.join(src, f) for f in B.SOURCES if os.path.exists(os.path.join(src, f))]
     subprocess.run(cmd, check=True, cwd=src)
     print(out)
 
