@@ -553,9 +553,14 @@ def run_ours(args):
             "peak_source": "profiles/l2_peak.json (tools/l2_peak.cu, L2-resident read kernel on a B200)",
             "bytes_per_step": "20 + 8*deg(s) (SURVEY.md §8d)", "alg_bytes_per_launch": alg_bytes_local,
             "walk_kernel_ms": walk_ms_rank0, "hbm_peak": hbm_peak,
-            "measured": ({k: ncu[k] for k in ("l2_bytes_per_launch", "dram_bytes_per_launch", "issue_active",
-                                              "ipc", "l2_frac_of_peak", "captured") if k in ncu} if ncu else
-                         "no ncu capture of this walk-kernel source (profiles/walk_traffic.json)"),
+            "measured": (dict({k: ncu[k] for k in ("l2_bytes_per_launch", "dram_bytes_per_launch", "issue_active",
+                                                   "ipc", "warp_instructions_per_launch", "l1_hit_rate",
+                                                   "l2_hit_rate", "captured") if k in ncu},
+                              l2_gbs=ncu["l2_bytes_per_launch"] / (walk_ms_rank0 / 1e3) / 1e9,
+                              l2_frac=(ncu["l2_bytes_per_launch"] / (walk_ms_rank0 / 1e3) / 1e9 / l2_peak)
+                              if l2_peak else None,
+                              dram_frac=ncu["dram_bytes_per_launch"] / (walk_ms_rank0 / 1e3) / 1e9 / hbm_peak)
+                         if ncu else "no ncu capture of this walk-kernel source (profiles/walk_traffic.json)"),
             "note": ("the model counts the whole CDF row (8*deg B) per step; the guide table reads ~1-2 "
                      "entries, so L2 moves ~1/3 of the model bytes (measured.l2_bytes_per_launch) and the "
                      "kernel is bound by SM instruction issue (measured.issue_active), not by L2 or HBM"),

@@ -234,20 +234,23 @@ int mcmi_partition_rows(const int64_t* row_ptr, int64_t row_begin, int64_t row_e
 /* The same build of rows [row_begin, row_end) started on a library thread, for
  * callers that size their own output while the walks run (the C++ drop-in,
  * include/mcmi/mcspai_compat.hpp): B's arrays must stay valid until
- * mcmi_job_finish.  mcmi_job_estimate blocks until the first row chunk (10% of
+ * mcmi_job_finish.  mcmi_job_estimate blocks until the first row chunk (5% of
  * the rows) is built and returns an upper-biased extrapolation of nnz(M)
- * (x1.06 + 1024; exact when the build has a single chunk), or -1 with the
- * build's error status if it failed first.  mcmi_job_finish waits for the
+ * (x1.08 + 1024; exact when the build has a single chunk or is over), or -1
+ * with the build's error status if it failed first; later calls return at once
+ * with the latest estimate (refreshed after every chunk, never lowered).  mcmi_job_finish waits for the
  * build and returns its result (to be freed with mcmi_result_free), or the
  * build's error; it frees the job. */
 typedef struct mcmi_job mcmi_job;
 int mcmi_build_start(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row_begin, int64_t row_end,
                      mcmi_job** job, char* err, size_t errlen);
 int mcmi_job_estimate(mcmi_job* job, int64_t* nnz_estimate);
-/* Hands the job the caller's entry arrays (capacity entries each, once per
- * job): from then on every row chunk is copied into them as soon as its
- * device->host copy completes, while later chunks still walk.  Entries beyond
- * `capacity` are not delivered (mcmi_result_copy_range copies them later). */
+/* Hands the job the caller's entry arrays, of which entries [0, capacity) may
+ * be written: from then on every row chunk is copied into them as soon as its
+ * device->host copy completes, while later chunks still walk.  May be called
+ * again with the same arrays and a larger capacity as the caller's storage
+ * grows.  Entries beyond `capacity` are not delivered (mcmi_result_copy_range
+ * copies them later). */
 int mcmi_job_attach(mcmi_job* job, int64_t* col_idx, double* values, int64_t capacity);
 /* *delivered (may be NULL) = the leading entries already in the attached
  * arrays; the rest is copied with mcmi_result_copy_range. */

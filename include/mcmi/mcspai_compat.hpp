@@ -30,13 +30,18 @@
 #ifndef MCMI_MCSPAI_COMPAT_HPP
 #define MCMI_MCSPAI_COMPAT_HPP
 
+#include <chrono>
 #include <cstddef>
 #include <cstdint>
+#include <cstdio>
+#include <cstdlib>
 #include <istream>
 #include <iterator>
 #include <ostream>
 #include <new>
 #include <stdexcept>
+#include <condition_variable>
+#include <mutex>
 #include <string>
 #include <thread>
 #include <vector>
@@ -91,12 +96,25 @@ template <class SplitErrorT>
 
 namespace detail {
 
-// Sizes a result vector while the GPU is still walking: reserve, then (Linux)
-// madvise(MADV_HUGEPAGE) on the untouched storage, then the value-initialising
-// resize.  2 MB pages make that first touch ~3x faster (tools/host_probe.cu on
-// the B200 box: 1.28 GB in 148 ms instead of 445 ms).
+// Sizing of the result's entry vectors while the GPU walks.  First-touching
+// fresh memory is the host's bottleneck (tools/host_probe.cu on the B200 box:
+// ~12.5 GB/s of page faults, 2 MB pages included; C2's two 1.28 GB vectors
+// take ~200 ms), so it starts with the build: each vector reserves a generous
+// virtual range (nothing touched), asks for 2 MB pages, and grows by
+// value-initialising resizes up to the current limit (16M entries until the
+// library's estimate is known, then the estimate), publishing its ready size;
+// the ready prefix is attached to the job, whose copier fills it as row chunks
+// land.  The data pointer never moves while size <= the reserved capacity.
+struct Presizer {
+    std::mutex mu;
+    std::condition_variable cv;
+    int64_t limit = int64_t{16} << 20;
+    bool limit_final = false, stop = false;
+    int64_t ready[2] = {0, 0};
+};
+
 template <class VecT>
-void presize(VecT& v, size_t count) {
+void reserve_huge(VecT& v, size_t count) {
     v.reserve(count);
 #ifdef __linux__
     const size_t bytes = count * sizeof(typename VecT::value_type);
@@ -106,19 +124,49 @@ void presize(VecT& v, size_t count) {
         if (e > a) madvise(reinterpret_cast<void*>(a), e - a, MADV_HUGEPAGE);
     }
 #endif
-    v.resize(count);
+}
+
+template <class VecT, class Publish, class Refresh>
+void grow_within(VecT& v, size_t reserved, int k, Presizer& p, Publish&& publish, Refresh&& refresh) {
+    const size_t step = size_t{16} << 20;  // 128 MB of entries per resize
+    for (;;) {
+        size_t target;
+        {
+            std::unique_lock<std::mutex> lk(p.mu);
+            for (;;) {
+                const size_t lim = static_cast<size_t>(std::min<int64_t>(p.limit, reserved));
+                if (p.stop) return;
+                if (v.size() < lim) {
+                    target = std::min(lim, v.size() + step);
+                    break;
+                }
+                if (p.limit_final) {  // caught up: poll the library's refreshed estimate
+                    lk.unlock();
+                    const int64_t e = refresh();
+                    lk.lock();
+                    if (e > p.limit) {
+                        p.limit = e;
+                        continue;
+                    }
+                }
+                p.cv.wait_for(lk, std::chrono::milliseconds(2));
+            }
+        }
+        v.resize(target);
+        publish(k, static_cast<int64_t>(target));
+    }
 }
 
 }  // namespace detail
 
 // The reference's compute_preconditioner on the B200 build.  The build runs on
 // a library thread (mcmi_build_start) and streams M into page-locked memory
-// chunk by chunk; as soon as the first row chunk gives an entry estimate
-// (mcmi_job_estimate), two host threads size the caller's std::vectors while
-// the GPU keeps walking, then the vectors are attached (mcmi_job_attach) and
-// every chunk is copied into them as it lands, so only the last chunks' copy
-// follows the build.  An estimate that falls short just costs a regrow; the
-// result never depends on it.
+// chunk by chunk.  Meanwhile two host threads grow the result's std::vectors
+// (detail::grow_within, sized by the library's early estimate,
+// mcmi_job_estimate) and attach their ready prefix to the job
+// (mcmi_job_attach), whose copier moves each landed chunk into them; only what
+// is left when the build ends is copied afterwards.  An estimate that falls
+// short just costs a regrow; the result never depends on it.
 template <class ApproxInverseT, class SplitErrorT, class CsrT, class CfgT>
 ApproxInverseT compute_preconditioner(const CsrT& b, const CfgT& cfg, const Options& opt = {}) {
     const mcmi_config c = to_config(cfg, opt);
@@ -126,43 +174,82 @@ ApproxInverseT compute_preconditioner(const CsrT& b, const CfgT& cfg, const Opti
                              reinterpret_cast<const int64_t*>(b.row_ptr.data()),
                              reinterpret_cast<const int64_t*>(b.col_idx.data()), b.values.data()};
     char err[512] = {0};
+    // MCMI_COMPAT_TRACE=1: phase timestamps of this call on stderr (tuning)
+    static const bool trace = std::getenv("MCMI_COMPAT_TRACE") != nullptr;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto mark = [&](const char* what) {
+        if (trace)
+            std::fprintf(stderr, "mcmi compat: %-10s %8.2f ms\n", what,
+                         std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+    };
     mcmi_job* job = nullptr;
     int code = mcmi_build_start(&view, &c, 0, -1, &job, err, sizeof err);
     if (code != MCMI_OK) rethrow<SplitErrorT>(code, err);
     ApproxInverseT out;
-    int64_t est = -1;
+    const int64_t nnz_b = b.n > 0 ? static_cast<int64_t>(b.row_ptr[b.n]) : 0;
+    const size_t reserved = static_cast<size_t>(std::min<int64_t>(std::max<int64_t>(nnz_b * 16, 1 << 20), int64_t{1} << 31));
+    detail::Presizer ps;
+    // until the estimate arrives, grow to nnz(B) entries: M holds every row's
+    // diagonal and, for any budget worth a GPU, more than B's pattern
+    ps.limit = std::max<int64_t>(ps.limit, std::min<int64_t>(nnz_b, static_cast<int64_t>(reserved)));
+    int64_t* col_ptr = nullptr;  // stable: the vectors never outgrow `reserved` while attached
+    double* val_ptr = nullptr;
+    auto publish = [&](int k, int64_t ready) {
+        std::lock_guard<std::mutex> lk(ps.mu);
+        ps.ready[k] = ready;
+        const int64_t both = std::min(ps.ready[0], ps.ready[1]);
+        if (both > 0) mcmi_job_attach(job, col_ptr, val_ptr, both);
+    };
+    auto refresh = [&] {  // the library's latest (never lowered) estimate
+        int64_t e = -1;
+        return mcmi_job_estimate(job, &e) == MCMI_OK ? e : int64_t{-1};
+    };
     std::thread sizers[2];
-    if (mcmi_job_estimate(job, &est) == MCMI_OK && est > 0) {
-        try {
-            sizers[0] = std::thread([&] { detail::presize(out.m.col_idx, static_cast<size_t>(est)); });
-            sizers[1] = std::thread([&] { detail::presize(out.m.values, static_cast<size_t>(est)); });
-        } catch (...) {  // no thread: the vectors are sized after the build
-        }
-    }
-    const int64_t rows = b.n > 0 ? static_cast<int64_t>(b.n) : 0;
-    std::vector<int64_t> chains, before;
     try {
-        out.m.row_ptr.resize(static_cast<size_t>(rows) + 1);
-        out.row_meta.resize(static_cast<size_t>(rows));
-        chains.resize(static_cast<size_t>(rows));
-        before.resize(static_cast<size_t>(rows));
-    } catch (...) {
+        detail::reserve_huge(out.m.col_idx, reserved);
+        detail::reserve_huge(out.m.values, reserved);
+        col_ptr = reinterpret_cast<int64_t*>(out.m.col_idx.data());
+        val_ptr = out.m.values.data();
+        sizers[0] = std::thread([&] { detail::grow_within(out.m.col_idx, reserved, 0, ps, publish, refresh); });
+        sizers[1] = std::thread([&] { detail::grow_within(out.m.values, reserved, 1, ps, publish, refresh); });
+    } catch (...) {  // no memory or no thread: the vectors are sized after the build
+    }
+    auto stop_sizers = [&] {
+        {
+            std::lock_guard<std::mutex> lk(ps.mu);
+            ps.stop = true;
+        }
+        ps.cv.notify_all();
         for (auto& t : sizers)
             if (t.joinable()) t.join();
+    };
+    int64_t est = -1;
+    const int est_code = mcmi_job_estimate(job, &est);
+    {
+        std::lock_guard<std::mutex> lk(ps.mu);
+        ps.limit = (est_code == MCMI_OK && est > 0) ? est : 0;
+        ps.limit_final = true;
+    }
+    ps.cv.notify_all();
+    mark("estimate");
+    const int64_t rows = b.n > 0 ? static_cast<int64_t>(b.n) : 0;
+    try {
+        detail::reserve_huge(out.m.row_ptr, static_cast<size_t>(rows) + 1);
+        detail::reserve_huge(out.row_meta, static_cast<size_t>(rows));
+        out.m.row_ptr.resize(static_cast<size_t>(rows) + 1);
+        out.row_meta.resize(static_cast<size_t>(rows));
+    } catch (...) {
+        stop_sizers();
         mcmi_job_finish(job, nullptr, nullptr, nullptr, 0);
         throw;
     }
-    bool sized = sizers[0].joinable() && sizers[1].joinable();
-    for (auto& t : sizers)
-        if (t.joinable()) t.join();
-    // the vectors are sized: chunks that already landed, and every later one,
-    // are copied into them while the walks go on
-    if (sized && out.m.col_idx.size() == static_cast<size_t>(est) && out.m.values.size() == static_cast<size_t>(est))
-        sized = mcmi_job_attach(job, reinterpret_cast<int64_t*>(out.m.col_idx.data()), out.m.values.data(), est) ==
-                MCMI_OK;
+    mark("meta sized");
     mcmi_result* res = nullptr;
     int64_t delivered = 0;
     code = mcmi_job_finish(job, &res, &delivered, err, sizeof err);
+    mark("built");
+    stop_sizers();
+    mark("presized");
     if (code != MCMI_OK) rethrow<SplitErrorT>(code, err);
     struct Guard {
         mcmi_result* r;
@@ -170,20 +257,23 @@ ApproxInverseT compute_preconditioner(const CsrT& b, const CfgT& cfg, const Opti
     } guard{res};
     int64_t n = 0, nnz = 0;
     mcmi_result_sizes(res, &n, &nnz);
-    if (!sized) delivered = 0;
     out.m.n = n;
     out.m.row_ptr.resize(static_cast<size_t>(n) + 1);
-    out.m.col_idx.resize(static_cast<size_t>(nnz));  // shrinks in place when the estimate held
+    out.m.col_idx.resize(static_cast<size_t>(nnz));  // shrinks in place, or grows keeping the delivered prefix
     out.m.values.resize(static_cast<size_t>(nnz));
-    chains.resize(static_cast<size_t>(n));
-    before.resize(static_cast<size_t>(n));
+    delivered = std::min(delivered, nnz);
     int64_t n_chains = 0, max_len = 0;
-    if (mcmi_result_copy(res, reinterpret_cast<int64_t*>(out.m.row_ptr.data()), nullptr, nullptr, chains.data(),
-                         before.data(), &n_chains, &max_len) != MCMI_OK ||
+    if (mcmi_result_copy(res, reinterpret_cast<int64_t*>(out.m.row_ptr.data()), nullptr, nullptr, nullptr, nullptr,
+                         &n_chains, &max_len) != MCMI_OK ||
         mcmi_result_copy_range(res, delivered, nnz, reinterpret_cast<int64_t*>(out.m.col_idx.data()),
                                out.m.values.data()) != MCMI_OK)
         throw std::runtime_error("mcmi: result copy failed");
+    mark("copied");
+    if (trace) std::fprintf(stderr, "mcmi compat: delivered %lld of %lld entries early\n",
+                            static_cast<long long>(delivered), static_cast<long long>(nnz));
     out.row_meta.resize(static_cast<size_t>(n));
+    const int64_t *chains = nullptr, *before = nullptr;  // RowMeta straight from the result's arrays
+    mcmi_result_view(res, nullptr, nullptr, nullptr, &chains, &before);
     for (int64_t i = 0; i < n; ++i) {
         out.row_meta[i].chains_used = chains[i];
         out.row_meta[i].entries_before_retention = before[i];
@@ -192,6 +282,7 @@ ApproxInverseT compute_preconditioner(const CsrT& b, const CfgT& cfg, const Opti
     out.budget_echo.n_chains = n_chains;
     out.budget_echo.max_len = max_len;
     out.seed_echo = cfg.master_seed;
+    mark("done");
     return out;
 }
 

@@ -934,9 +934,14 @@ Status build_from_host(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config
     auto h2d = [&](void* dst, const void* src, size_t bytes) {
         if (st.code == MCMI_OK && bytes) st = cuda_status(stage_h2d(dst, src, bytes, s), "H2D");
     };
+    const auto hs0 = std::chrono::steady_clock::now();
     h2d(d_rp, b.row_ptr, (n + 1) * sizeof(int64_t));
     h2d(d_ci, b.col_idx, nnz * sizeof(int64_t));
     h2d(d_v, b.values, nnz * sizeof(double));
+    if (getenv("MCMI_STREAM_DEBUG"))
+        std::fprintf(stderr, "mcmi stage B: %.2f ms host (%lld bytes)\n",
+                     std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hs0).count(),
+                     static_cast<long long>((n + 1 + 2 * nnz) * 8));
     if (ap_host) h2d(d_p, ap_host->p_values, nnz * sizeof(double));
     if (st.code == MCMI_OK) {
         const mcmi_csr_view dv{n, static_cast<int64_t*>(d_rp), static_cast<int64_t*>(d_ci),
@@ -1008,49 +1013,60 @@ struct mcmi_job {
         int64_t lo, hi;
         cudaEvent_t ev;
     };
-    std::deque<Range> landed;       // queued chunk copies, in entry order
+    std::deque<Range> landed;       // queued chunk copies (device -> page-locked), in entry order
+    int64_t landed_hi = 0;          // entries [0, landed_hi) are in the result's host arrays
     std::thread copier;
     bool build_over = false;        // no more ranges will be queued
     bool growing = false, busy = false;
     int64_t* dst_col = nullptr;
     double* dst_val = nullptr;
-    int64_t dst_cap = 0;
+    int64_t dst_cap = 0;            // entries [0, dst_cap) of the attached arrays may be written
     int64_t delivered = 0;          // entries [0, delivered) are in the attached arrays
     const int64_t* src_col = nullptr;  // the result's current page-locked arrays
     const double* src_val = nullptr;
 
+    int64_t deliverable() const { return dst_col ? std::min(landed_hi, dst_cap) : 0; }
     void copier_loop() {
         for (;;) {
-            Range rg{};
-            const int64_t* sc;
-            const double* sv;
-            int64_t* dc;
-            double* dv;
+            cudaEvent_t ev = nullptr;
+            int64_t rhi = 0, a0 = 0, a1 = 0;
+            const int64_t* sc = nullptr;
+            const double* sv = nullptr;
+            int64_t* dc = nullptr;
+            double* dv = nullptr;
             {
                 std::unique_lock<std::mutex> lk(mu);
                 cv.wait(lk, [&] {
-                    return (!landed.empty() && dst_col && !growing) || (build_over && (landed.empty() || !dst_col));
+                    return !growing && (!landed.empty() || delivered < deliverable() || build_over);
                 });
-                if (landed.empty() || !dst_col) return;  // the build thread destroys any events left
-                rg = landed.front();
-                landed.pop_front();
-                busy = true;
-                sc = src_col;
-                sv = src_val;
-                dc = dst_col;
-                dv = dst_val;
+                if (!landed.empty()) {
+                    ev = landed.front().ev;
+                    rhi = landed.front().hi;
+                    landed.pop_front();
+                } else if (delivered < deliverable()) {
+                    a0 = delivered;
+                    a1 = deliverable();
+                    busy = true;
+                    sc = src_col;
+                    sv = src_val;
+                    dc = dst_col;
+                    dv = dst_val;
+                } else {
+                    return;  // the build is over and everything landed so far is delivered
+                }
             }
-            const bool ok = cudaEventSynchronize(rg.ev) == cudaSuccess;
-            cudaEventDestroy(rg.ev);
-            const int64_t hi_c = std::min(rg.hi, dst_cap);
-            bool advanced = false;
-            if (ok && rg.lo == delivered && hi_c > rg.lo) {  // ranges arrive in order
-                parallel_copy(dc + rg.lo, sc + rg.lo, static_cast<size_t>(hi_c - rg.lo) * sizeof(int64_t));
-                parallel_copy(dv + rg.lo, sv + rg.lo, static_cast<size_t>(hi_c - rg.lo) * sizeof(double));
-                advanced = true;
+            if (ev) {  // a chunk's device->host copy: wait for it, then it is deliverable
+                const bool ok = cudaEventSynchronize(ev) == cudaSuccess;
+                cudaEventDestroy(ev);
+                std::lock_guard<std::mutex> lk(mu);
+                if (ok) landed_hi = std::max(landed_hi, rhi);
+                cv.notify_all();
+                continue;
             }
+            parallel_copy(dc + a0, sc + a0, static_cast<size_t>(a1 - a0) * sizeof(int64_t));
+            parallel_copy(dv + a0, sv + a0, static_cast<size_t>(a1 - a0) * sizeof(double));
             std::lock_guard<std::mutex> lk(mu);
-            if (advanced) delivered = hi_c;
+            delivered = a1;
             busy = false;
             cv.notify_all();
         }
@@ -1345,13 +1361,13 @@ Status build_host(const mcmi_csr_view& b, const mcmi_config& cfg, int64_t lo, in
             job->cv.notify_all();
         };
     }
-    bool published = false;
+    // the estimate is refreshed after every chunk (the first rows of a stencil
+    // are a boundary and under-represent the rest)
     sink.progress = [&](int64_t done, int64_t nnz_so_far, int64_t total) {
-        if (published || !on_estimate) return;
-        published = true;
+        if (!on_estimate) return;
         on_estimate(done >= total ? nnz_so_far
                                   : static_cast<int64_t>(static_cast<double>(nnz_so_far) * total /
-                                                         static_cast<double>(std::max<int64_t>(done, 1)) * 1.06) +
+                                                         static_cast<double>(std::max<int64_t>(done, 1)) * 1.08) +
                                         1024);
     };
     mcmi_device_csr dc{};
@@ -1778,15 +1794,13 @@ int mcmi_build_start(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row
             auto* r = new mcmi_result();
             auto publish = [j](int64_t est) {
                 std::lock_guard<std::mutex> lk(j->mu);
-                if (!j->has_estimate) {
-                    j->has_estimate = true;
-                    j->estimate = est;
-                }
+                j->estimate = j->has_estimate ? std::max(j->estimate, est) : est;  // never lowered
+                j->has_estimate = true;
                 j->cv.notify_all();
             };
-            // a small first chunk (10% of the rows) gives the caller its entry
+            // a small first chunk (5% of the rows) gives the caller its entry
             // estimate early enough to size its own arrays while the walks run
-            const Status st = build_host(j->b, j->cfg, j->lo, j->hi, r, publish, 0.1, nullptr, j);
+            const Status st = build_host(j->b, j->cfg, j->lo, j->hi, r, publish, 0.05, nullptr, j);
             {
                 std::lock_guard<std::mutex> lk(j->mu);
                 j->build_over = true;
@@ -1799,9 +1813,9 @@ int mcmi_build_start(const mcmi_csr_view* b, const mcmi_config* cfg, int64_t row
             if (st.code) {
                 delete r;
                 r = nullptr;
-            } else if (!j->has_estimate) {
+            } else {
                 j->has_estimate = true;
-                j->estimate = r->nnz;
+                j->estimate = r->nnz;  // exact once built
             }
             j->code = st.code;
             j->msg = st.msg;
@@ -1836,11 +1850,11 @@ int mcmi_job_estimate(mcmi_job* job, int64_t* nnz_estimate) {
 int mcmi_job_attach(mcmi_job* job, int64_t* col_idx, double* values, int64_t capacity) {
     if (!job || (capacity > 0 && (!col_idx || !values))) return MCMI_EINVAL;
     std::lock_guard<std::mutex> lk(job->mu);
-    if (job->dst_col) return MCMI_EINVAL;  // once per job
     if (capacity <= 0) return MCMI_OK;
+    if (job->dst_col && (job->dst_col != col_idx || job->dst_val != values)) return MCMI_EINVAL;  // same arrays
     job->dst_col = col_idx;
     job->dst_val = values;
-    job->dst_cap = capacity;
+    job->dst_cap = std::max(job->dst_cap, capacity);  // the caller's arrays grow while the build runs
     job->cv.notify_all();
     return MCMI_OK;
 }
