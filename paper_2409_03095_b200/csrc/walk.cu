@@ -140,9 +140,9 @@ __device__ __forceinline__ int hash_slot(int* keys, unsigned mask, int shift, in
 // an exactly representable multiple of ulp(acc), so those additions collapse
 // into one exact addition; the addition that crosses 2^(e+1) is performed on
 // its own (it may round).  A run therefore costs O(binade crossings), not O(k).
-__device__ __forceinline__ double add_ones_slow(double acc, int k) {
-    // an integer-valued acc (no return weight added yet) stays exact
-    if (acc == floor(acc) && fabs(acc) + static_cast<double>(k) < 0x1.0p53) return acc + static_cast<double>(k);
+// Out of line: taken a few times per row (the row start, two-binade runs), and
+// inlined the compiler if-converts part of it into the fast path.
+__device__ __noinline__ double add_ones_slow(double acc, int k) {
     while (k > 0) {
         if (!(acc >= 1.0 && acc < 0x1.0p53)) {  // acc == 0 (row start) or out of range
             acc += 1.0;
@@ -462,6 +462,14 @@ constexpr int kNbBytes = 32 + 2 * kNbDeg + kNbDeg + kNbT2;  // mask[8] u32, off[
 // the log covers the step-1 deposits alone (one 32-entry chunk per batch
 // instead of two), and c_k's sums are formed once per row.  Bit-identical.
 constexpr int kTfBytes = 32 * 4;  // per-warp m_k counters (deg(r) <= 16)
+
+// L = 2 deposit-log swizzle: deposit (chain j, step t) of a 32-chain batch sits
+// at t*32 + (j ^ 16t) in log_col and t*32 + (j ^ 8t) in log_w, so both the
+// walk's writes (one step, all chains) and the fold's chain-major reads (16
+// chains x 2 steps per 32-entry chunk) are bank-conflict free: the int reads
+// cover banks 0-31 once, and each half-warp's 8-byte reads cover them once.
+__device__ __forceinline__ int lf2_col_at(int t, int j) { return t * 32 + (j ^ (t << 4)); }
+__device__ __forceinline__ int lf2_w_at(int t, int j) { return t * 32 + (j ^ (t << 3)); }
 template <int LF, bool NB>
 __host__ __device__ constexpr bool split_fold_kernel() {
     return LF == 2 && !NB;
@@ -761,8 +769,13 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 if (kTF && tf && t == 0) {
                     k1 = static_cast<int>(kidx);  // counted, not logged (split fold)
                 } else {
-                    lc[mi * B] = logv;
-                    lw[mi * B] = w;
+                    if (LF == 2) {
+                        sm.log_col[lf2_col_at(t, lane)] = logv;
+                        sm.log_w[lf2_w_at(t, lane)] = w;
+                    } else {
+                        lc[mi * B] = logv;
+                        lw[mi * B] = w;
+                    }
                 }
                 ++m;
                 if (logv == rkey) {
@@ -775,7 +788,8 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             }
 
             if (active)
-                for (int t1 = m; t1 < S; ++t1) lc[t1 * B] = -1;  // end-of-chain sentinel for the fold
+                for (int t1 = m; t1 < S; ++t1)  // end-of-chain sentinel for the fold
+                    lc[LF == 2 ? lf2_col_at(t1, lane) - lane : t1 * B] = -1;
             if (__any_sync(FULL_MASK, log_full)) {  // longer walks: retry the row on a longer log
                 overflow = true;
                 break;
@@ -915,7 +929,8 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 bool ok = p < span && ((valid >> j) & 1u);
                 // chain-major position p -> step-major slot
                 const int q = (kTF && tf) ? B + j : (p - j * S) * B + j;
-                int c = ok ? sm.log_col[q] : -1;
+                const int tq = (kTF && tf) ? 1 : p - j * S;  // step of position p
+                int c = ok ? sm.log_col[LF == 2 ? lf2_col_at(tq, j) : q] : -1;
                 ok = ok && c >= 0 && c != rkey;  // column r was folded in (i)
                 if (!ok) c = -1 - lane;          // unique non-column tag
                 const unsigned peers = __match_any_sync(FULL_MASK, c);
@@ -939,7 +954,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 }
                 if (NB && nb) slot = ok ? c : 0;  // the logged key is the slot
                 else slot = __shfl_sync(FULL_MASK, slot, leader);
-                const double w = ok ? sm.log_w[q] : 0.0;
+                const double w = ok ? sm.log_w[LF == 2 ? lf2_w_at(tq, j) : q] : 0.0;
                 double v = w;
                 if (ok && rank == 0 && slot >= 0) v = sm.vals[slot] + w;
                 const int maxsize = __reduce_max_sync(FULL_MASK, static_cast<unsigned>(gsize));
