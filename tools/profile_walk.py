@@ -17,6 +17,8 @@ def main():
     p.add_argument("--rng", default="reference", choices=["reference", "keyed"])
     p.add_argument("--rows", type=int, default=-1, help="build only the first ROWS rows")
     p.add_argument("--repeat", type=int, default=2)
+    p.add_argument("--chains", type=int, default=None, help="chains_override (C5 grid points)")
+    p.add_argument("--len", type=int, default=None, help="max_len_override (C5 grid points)")
     a = p.parse_args()
     import torch
     from paper_2409_03095_b200 import generators as G
@@ -24,6 +26,11 @@ def main():
     from paper_2409_03095_b200.mcspai import McConfig, RngMode
     gen, over = G.CONFIGS[a.config]
     b = gen()
+    over = dict(over)
+    if a.chains is not None:
+        over["chains_override"] = a.chains
+    if a.len is not None:
+        over["max_len_override"] = a.len
     cfg = McConfig(**over, rng_mode=RngMode.reference if a.rng == "reference" else RngMode.keyed)
     eng = DeviceEngine(0)
     rp, ci, v = DeviceEngine.upload(b)
