@@ -916,33 +916,20 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             // as a shuffle chain in lane (= chain-major) order.
             int n_new = 0;
             bool fail = false;
-            // Positions run over the valid chains only (the v-th valid chain's
-            // steps at v*S ..): a partial last batch or a sparse reference-stream
-            // orbit folds in as few 32-entry chunks as it has deposits.  The
-            // split fold takes only the step-1 deposits (position v = chain v, step 1).
-            const int nvalid = __popc(valid);
-            const bool prefix = (valid & (valid + 1u)) == 0u;  // valid chains are lanes 0 .. nvalid-1
-            const int span = (kTF && tf) ? nvalid : nvalid * S;
+            // split fold: only the step-1 deposits (position p = chain j, step 1)
+            const int span = (kTF && tf) ? B : B * S;
             for (int base = 0; base < span; base += 32) {
                 const int p = base + lane;
-                // valid-chain index of position p: p / S (shift for power-of-two S, else the magic multiply)
-                const int vi = (kTF && tf) ? p
-                                           : (s_shift >= 0 ? (p >> s_shift)
-                                                           : static_cast<int>(
-                                                                 __umulhi(static_cast<unsigned>(p), a.log_magic)));
-                // its lane: vi itself for a prefix, else the vi-th set bit of valid
-                int j = min(vi, 31);
-                if (!prefix) {
-                    int pos = 0;  // largest b with popc(valid & ((1 << b) - 1)) <= vi
-#pragma unroll
-                    for (int sh = 16; sh; sh >>= 1)
-                        if (__popc(valid & ((1u << (pos + sh)) - 1u)) <= vi) pos += sh;
-                    j = pos;
-                }
-                bool ok = p < span;
+                // chain of position p: p / S (shift for power-of-two S, else the magic multiply)
+                const int j = (kTF && tf) ? p
+                                          : min(s_shift >= 0 ? (p >> s_shift)
+                                                             : static_cast<int>(
+                                                                   __umulhi(static_cast<unsigned>(p), a.log_magic)),
+                                                31);
+                bool ok = p < span && ((valid >> j) & 1u);
                 // chain-major position p -> step-major slot
-                const int tq = (kTF && tf) ? 1 : p - vi * S;  // step of position p
-                const int q = tq * B + j;
+                const int q = (kTF && tf) ? B + j : (p - j * S) * B + j;
+                const int tq = (kTF && tf) ? 1 : p - j * S;  // step of position p
                 int c = ok ? sm.log_col[LF == 2 ? lf2_col_at(tq, j) : q] : -1;
                 ok = ok && c >= 0 && c != rkey;  // column r was folded in (i)
                 if (!ok) c = -1 - lane;          // unique non-column tag
