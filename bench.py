@@ -360,16 +360,18 @@ def run_ours(args):
         torch.cuda.synchronize()
 
     def timed(step, k):
-        """k steps between barriers, CUDA events on the launching stream; max over ranks."""
+        """k steps between barriers, CUDA events on the launching stream; max over
+        ranks.  Returns (ms per step, [stats of each step], last step's output)."""
         barrier()
         ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        out = []
+        st, last = [], None
         ev0.record(stream)
         for _ in range(k):
-            out.append(step())
+            last = step()  # only the last M is kept (an all-gathered M is the whole matrix)
+            st.append(last[0].stats)
         ev1.record(stream)
         barrier()
-        return ev0.elapsed_time(ev1) / max(k, 1), out
+        return ev0.elapsed_time(ev1) / max(k, 1), st, last
 
     def reduce(vals, op):
         t = torch.tensor(vals, dtype=torch.float64, device=device)
@@ -401,8 +403,7 @@ def run_ours(args):
     for _ in range(max(args.warmup, 0)):
         step()
     with ClockSampler(local) as clk:
-        ms_local, outs = timed(step, args.steps)
-    stats = [d.stats for d, _ in outs]
+        ms_local, stats, last = timed(step, args.steps)
     steps_local = sum(s["walk_steps"] for s in stats) / max(args.steps, 1)
     walk_ms_local = sum(s["ms_walk_kernel"] for s in stats) / max(args.steps, 1)
     launches_local = sum(s["launches"] for s in stats) + (args.steps if assembly == "p2p" else 0)
@@ -411,7 +412,7 @@ def run_ours(args):
     value = total_steps / (ms_per_step / 1e3)
 
     # the M of the last timed build, hashed on rank 0 (outside the timed region)
-    d_last, m_last = outs[-1]
+    d_last, m_last = last
     if world == 1:
         rp_t, ci_t, v_t, _, _ = eng.to_tensors(d_last, stream=stream)
     else:
@@ -422,7 +423,7 @@ def run_ours(args):
         m_host = (rp_t.cpu().numpy(), ci_t.cpu().numpy(), v_t.cpu().numpy())
         m_sha, m_sum = csr_sha256(*m_host), positional_checksum(*m_host)
         del m_host
-    del outs, rp_t, ci_t, v_t
+    del last, m_last, rp_t, ci_t, v_t
     b_sha = csr_sha256(b.row_ptr, b.col_idx, b.values) if rank == 0 else None
     g = golden(args.config, b_sha) if rank == 0 else None
 
@@ -433,11 +434,10 @@ def run_ours(args):
         kcfg.rng_mode = RngMode.keyed
         kstep = make_step(b, kcfg, lo, hi, dv)
         kstep()
-        kms, kout = timed(kstep, 3)
+        kms, kst, _ = timed(kstep, 3)
         (kms,) = reduce([kms], "max")
-        (ksteps,) = reduce([kout[-1][0].stats["walk_steps"]], "sum")
+        (ksteps,) = reduce([kst[-1]["walk_steps"]], "sum")
         alt = {"rng_mode": "keyed", "value": ksteps / (kms / 1e3), "ms_per_step": kms}
-        del kout
 
     # algorithmic bytes per build: 20*steps + 8*sum deg(s); the
     # sum of degrees comes from one extra, untimed build with MCMI_FLAG_DEG_STATS
@@ -458,12 +458,12 @@ def run_ours(args):
             xstep = make_step(xb, xcfg, xlo, xhi, xdv)
             for _ in range(2):
                 xstep()
-            xms, xout = timed(xstep, 5)
-            xs = xout[-1][0].stats
+            xms, xst, _ = timed(xstep, 5)
+            xs = xst[-1]
             (xms, xwalk), (xsteps,) = reduce([xms, xs["ms_walk_kernel"]], "max"), reduce([xs["walk_steps"]], "sum")
             extra[name] = {"build_ms": xms, "walk_kernel_ms": xwalk, "walk_steps": int(xsteps),
                            "value": xsteps / (xms / 1e3), "n_chains": xs["n_chains"], "max_len": xs["max_len"]}
-            del xout, xdv
+            del xdv
 
     # ---- end to end through the public API: pinned host CSR in, host M out.
     # N = 1: compute_preconditioner(B) (streamed build into library-owned pinned
@@ -479,6 +479,9 @@ def run_ours(args):
         ecfg = McConfig(**{k: getattr(cfg, k) for k in cfg.__dataclass_fields__})
         ecfg.device, ecfg.n_gpus = 0, world
         times, st = [], None
+        # ranks != 0 wait on the store, not in an NCCL barrier: a barrier kernel
+        # spinning on their GPUs would share the SMs rank 0's build runs on
+        store = dist.distributed_c10d._get_default_store() if world > 1 else None
         if rank == 0:
             r = compute_preconditioner(hb, ecfg)  # warm-up
             del r
@@ -490,6 +493,11 @@ def run_ours(args):
                 e2e_nnz = r.m.nnz()
                 del r
         if world > 1:
+            if rank == 0:
+                store.set("mcmi_e2e_done", "1")
+            else:
+                import datetime
+                store.wait(["mcmi_e2e_done"], datetime.timedelta(seconds=900))
             dist.barrier()
         if rank == 0:
             t_e2e = statistics.mean(times)

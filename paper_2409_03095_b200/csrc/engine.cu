@@ -478,7 +478,22 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         if (first_cap < 256 && tiers.back().cap_limit < bound) tiers.push_back(make_tier(256, L));
         if (tiers.back().cap_limit < bound) tiers.push_back(make_global_tier(0, L, 1024));
     }
-    if (tiers.empty() || tiers.back().cap_limit < bound) tiers.push_back(make_global_tier(bound, L));
+    // Global tiers grow x8 up to the one sized to the bound: a row lands in a
+    // table within 8x of its distinct columns, so huge bounds (C5's 10^4 x 32
+    // corner: bound 3.2e5, rows of far fewer columns) do not give every warp
+    // a multi-MB table (fewer resident warps, a finalize scan of cap slots).
+    {
+        int64_t gcap = (!tiers.empty() && tiers.back().global) ? int64_t{tiers.back().cap} * 8 : 8192;
+        while (tiers.empty() || tiers.back().cap_limit < bound) {
+            const Tier t = make_global_tier(0, L, gcap);
+            if (t.cap_limit >= bound || gcap >= (int64_t{1} << 27)) {
+                tiers.push_back(make_global_tier(bound, L));  // the smallest table holding the bound
+                break;
+            }
+            tiers.push_back(t);
+            gcap *= 8;
+        }
+    }
     st.hash_cap = first_cap;  // updated below if the pilot starts on a larger tier
 
     MCMI_TRY(e->row_cnt.ensure(std::max<int64_t>(rows, 1) * sizeof(int)), "alloc row_cnt");
@@ -564,9 +579,16 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
                 // cudaMemGetInfo (it can stall for tens of ms behind the driver)
                 max_warps = full;
             } else {
+                // Global-tier tables are latency-bound (random probes into HBM),
+                // so resident warps are throughput: up to half of the free
+                // memory, 64 GB (MCMI_SCRATCH_GB), is scratch.  Cached in the engine.
+                static const size_t budget_max = [] {
+                    const char* v = getenv("MCMI_SCRATCH_GB");
+                    return (v && *v ? static_cast<size_t>(std::max(1, atoi(v))) : size_t{64}) << 30;
+                }();
                 size_t free_b = 0, total_b = 0;
                 MCMI_TRY(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-                const size_t budget = std::min<size_t>(size_t{16} << 30, (free_b + e->gscratch.cap) / 2);
+                const size_t budget = std::min<size_t>(budget_max, (free_b + e->gscratch.cap) / 2);
                 max_warps = std::min<int64_t>(static_cast<int64_t>(budget / per_warp), full);
                 if (max_warps < 1) return fail(MCMI_ENOMEM, "accumulator row too large for device memory");
                 max_warps = std::max<int64_t>(8, max_warps / 8 * 8);
@@ -930,19 +952,20 @@ Status build_from_host(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config
     MCMI_TRY(cudaMallocAsync(&d_v, std::max<int64_t>(nnz, 1) * sizeof(double), s), "alloc B");
     Status st;
     // pageable inputs (a reference caller's std::vector) go through pinned
-    // bounce buffers: 11 GB/s -> ~50 GB/s on the box (hostio.h)
-    auto h2d = [&](void* dst, const void* src, size_t bytes) {
-        if (st.code == MCMI_OK && bytes) st = cuda_status(stage_h2d(dst, src, bytes, s), "H2D");
-    };
+    // bounce buffers in one pipeline: 11 GB/s -> ~40 GB/s on the box (hostio.h)
     const auto hs0 = std::chrono::steady_clock::now();
-    h2d(d_rp, b.row_ptr, (n + 1) * sizeof(int64_t));
-    h2d(d_ci, b.col_idx, nnz * sizeof(int64_t));
-    h2d(d_v, b.values, nnz * sizeof(double));
+    {
+        const H2DSegment segs[4] = {{d_rp, b.row_ptr, static_cast<size_t>(n + 1) * sizeof(int64_t)},
+                                    {d_ci, b.col_idx, static_cast<size_t>(nnz) * sizeof(int64_t)},
+                                    {d_v, b.values, static_cast<size_t>(nnz) * sizeof(double)},
+                                    {d_p, ap_host ? ap_host->p_values : nullptr,
+                                     ap_host ? static_cast<size_t>(nnz) * sizeof(double) : 0}};
+        st = cuda_status(stage_h2d(segs, 4, s), "H2D");
+    }
     if (getenv("MCMI_STREAM_DEBUG"))
         std::fprintf(stderr, "mcmi stage B: %.2f ms host (%lld bytes)\n",
                      std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - hs0).count(),
                      static_cast<long long>((n + 1 + 2 * nnz) * 8));
-    if (ap_host) h2d(d_p, ap_host->p_values, nnz * sizeof(double));
     if (st.code == MCMI_OK) {
         const mcmi_csr_view dv{n, static_cast<int64_t*>(d_rp), static_cast<int64_t*>(d_ci),
                                static_cast<double*>(d_v)};

@@ -163,11 +163,12 @@ class CopyPool {
 
 }  // namespace
 
-void parallel_copy(void* dst, const void* src, size_t bytes) {
+void parallel_copy(void* dst, const void* src, size_t bytes, int max_threads) {
     if (!bytes || dst == src) return;
     const size_t per = size_t{8} << 20;
     CopyPool& pool = CopyPool::get();
-    const size_t t = std::min<size_t>(pool.workers() + 1, (bytes + per - 1) / per);
+    const size_t t = std::min<size_t>({pool.workers() + 1, (bytes + per - 1) / per,
+                                       static_cast<size_t>(std::max(1, max_threads))});
     if (t <= 1) {
         std::memcpy(dst, src, bytes);
         return;
@@ -190,40 +191,52 @@ bool is_dma_ready(const void* p) {
     return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
-cudaError_t stage_h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
-    if (!bytes) return cudaSuccess;
-    const size_t chunk = size_t{64} << 20;
-    if (bytes <= (size_t{4} << 20) || is_dma_ready(src))
-        return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s);
-    // two bounce buffers, released to the pool once their DMAs have completed
-    PinnedBuf bb[2] = {pinned_acquire(chunk), pinned_acquire(chunk)};
-    cudaEvent_t ev[2] = {nullptr, nullptr};
+cudaError_t stage_h2d(const H2DSegment* segs, int nseg, cudaStream_t s) {
+    constexpr int kB = 2;                        // bounce buffers
+    constexpr size_t kChunk = size_t{64} << 20;  // per host copy / DMA
+    constexpr int kThreads = 16;  // the caller's own threads also fault its result pages meanwhile
     cudaError_t e = cudaSuccess;
-    if (!bb[0].p || !bb[1].p) e = cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, s);  // no pinned memory
-    for (int i = 0; i < 2 && e == cudaSuccess && bb[0].p && bb[1].p; ++i)
-        e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
-    if (e == cudaSuccess && bb[0].p && bb[1].p) {
-        bool used[2] = {false, false};
-        for (size_t off = 0, i = 0; off < bytes && e == cudaSuccess; off += chunk, ++i) {
-            const int k = static_cast<int>(i & 1);
-            const size_t len = std::min(chunk, bytes - off);
+    bool any_pageable = false;
+    for (int i = 0; i < nseg && e == cudaSuccess; ++i) {
+        if (!segs[i].bytes) continue;
+        if (segs[i].bytes <= (size_t{4} << 20) || is_dma_ready(segs[i].src))
+            e = cudaMemcpyAsync(segs[i].dst, segs[i].src, segs[i].bytes, cudaMemcpyDefault, s);
+        else
+            any_pageable = true;
+    }
+    if (e != cudaSuccess || !any_pageable) return e;
+    PinnedBuf bb[kB];
+    bool have = true;
+    for (auto& x : bb) have = have && (x = pinned_acquire(kChunk)).p != nullptr;
+    cudaEvent_t ev[kB] = {};
+    for (int i = 0; i < kB && have && e == cudaSuccess; ++i) e = cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming);
+    bool used[kB] = {};
+    int k = 0;
+    for (int i = 0; i < nseg && e == cudaSuccess; ++i) {
+        const H2DSegment& g = segs[i];
+        if (!g.bytes || g.bytes <= (size_t{4} << 20) || is_dma_ready(g.src)) continue;
+        if (!have) {  // no pinned memory: the driver's own (slower) pageable path
+            e = cudaMemcpyAsync(g.dst, g.src, g.bytes, cudaMemcpyDefault, s);
+            continue;
+        }
+        for (size_t off = 0; off < g.bytes && e == cudaSuccess; off += kChunk, k = (k + 1) % kB) {
+            const size_t len = std::min(kChunk, g.bytes - off);
             if (used[k]) e = cudaEventSynchronize(ev[k]);  // its previous DMA is done
             if (e != cudaSuccess) break;
-            parallel_copy(bb[k].p, static_cast<const unsigned char*>(src) + off, len);
-            e = cudaMemcpyAsync(static_cast<unsigned char*>(dst) + off, bb[k].p, len, cudaMemcpyHostToDevice, s);
+            parallel_copy(bb[k].p, static_cast<const unsigned char*>(g.src) + off, len, kThreads);
+            e = cudaMemcpyAsync(static_cast<unsigned char*>(g.dst) + off, bb[k].p, len, cudaMemcpyHostToDevice, s);
             if (e == cudaSuccess) e = cudaEventRecord(ev[k], s);
             used[k] = true;
         }
-        for (int k = 0; k < 2; ++k)
-            if (used[k]) {
-                const cudaError_t w = cudaEventSynchronize(ev[k]);
-                if (e == cudaSuccess) e = w;
-            }
     }
+    for (int j = 0; j < kB; ++j)
+        if (used[j]) {
+            const cudaError_t w = cudaEventSynchronize(ev[j]);
+            if (e == cudaSuccess) e = w;
+        }
     for (auto& x : ev)
         if (x) cudaEventDestroy(x);
-    pinned_release(bb[0]);
-    pinned_release(bb[1]);
+    for (auto& x : bb) pinned_release(x);
     return e;
 }
 
