@@ -182,6 +182,7 @@ __device__ __forceinline__ double add_ones(double acc, int k) {
     const double t = acc + static_cast<double>(k);
     // 1 <= acc < 2^50 (sign bit clear): one unsigned range test on the high word
     if (static_cast<unsigned>(hi - 0x3ff00000) < 0x03200000u && t < top2) return t;
+    if (acc == 0.0) return static_cast<double>(k);  // a row's start: 0 + 1 + ... + 1 = k exactly
     return add_ones_slow(acc, k);
 }
 
@@ -731,21 +732,18 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                     const unsigned gw = mb < 8 ? (mb < 4 ? r0.z : r0.w) : (mb < 12 ? r1.x : r1.y);
                     const unsigned g = (gw >> ((mb & 3) * 8)) & 0xffu;
                     unsigned q = r0.x + g * r1.w;  // r1.w = guide scale ceil(deg / 255)
-                    unsigned k;
-                    for (;; q += 2) {
-                        const double2 e0 = ent[q];
-                        const double2 e1 = ent[q + 1];  // past the row only when e0 is its +inf entry
-                        if (u < e0.x) {
-                            k = q;
-                            ratio = e0.y;
-                            break;
-                        }
-                        if (u < e1.x) {
-                            k = q + 1;
-                            ratio = e1.y;
-                            break;
-                        }
+                    // the first pair resolves almost every draw (16 guide buckets):
+                    // selects, not a loop, in the common case
+                    double2 e0 = ent[q];
+                    double2 e1 = ent[q + 1];  // past the row only when e0 is its +inf entry
+                    while (!(u < e0.x) && !(u < e1.x)) {
+                        q += 2;
+                        e0 = ent[q];
+                        e1 = ent[q + 1];
                     }
+                    const bool first_of_pair = u < e0.x;
+                    const unsigned k = first_of_pair ? q : q + 1;
+                    ratio = first_of_pair ? e0.y : e1.y;
                     kidx = k - r0.x;
                     if (!(NB && nb && t == 1)) nxt = tcol[k];  // NB: the last step logs a slot only
                 }
@@ -787,9 +785,13 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 if (fabs(w) < a.delta) alive = false;  // mc_engine.cpp:97
             }
 
-            if (active)
-                for (int t1 = m; t1 < S; ++t1)  // end-of-chain sentinel for the fold
-                    lc[LF == 2 ? lf2_col_at(t1, lane) - lane : t1 * B] = -1;
+            if (LF) {  // end-of-chain sentinels for the fold: predicated stores, no loop
+#pragma unroll
+                for (int t1 = 0; t1 < (LF ? LF : 1); ++t1)
+                    if (active && t1 >= m) lc[LF == 2 ? lf2_col_at(t1, lane) - lane : t1 * B] = -1;
+            } else if (active) {
+                for (int t1 = m; t1 < S; ++t1) lc[t1 * B] = -1;
+            }
             if (__any_sync(FULL_MASK, log_full)) {  // longer walks: retry the row on a longer log
                 overflow = true;
                 break;
