@@ -408,6 +408,7 @@ __device__ int sort_by_column(int* keys, double* vals, int s) {
         const int kk = lane < s ? keys[lane] : INT_MAX;
         const double vv = lane < s ? vals[lane] : 0.0;
         int pos = 0;
+#pragma unroll 4
         for (int j = 0; j < s; ++j) pos += __shfl_sync(FULL_MASK, kk, j) < kk;
         __syncwarp();
         if (lane < s) {
@@ -861,8 +862,9 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             if (kTF && tf) {
                 const bool took0 = mine && m >= 1;
                 const unsigned pk = __match_any_sync(FULL_MASK, took0 ? k1 : -1 - lane);
+                // ordered before the next batch's updates and the row-end read
+                // by the fold's __syncwarp()s
                 if (took0 && (pk & lt_mask) == 0) tf_cnt[k1] += __popc(pk);
-                __syncwarp();
             }
             // ------------------------------------- ordered (chain, step) fold
             // (i) column r: W0 = +1.0 per valid chain plus its returns, in
@@ -960,6 +962,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 double v = w;
                 if (ok && rank == 0 && slot >= 0) v = sm.vals[slot] + w;
                 const int maxsize = __reduce_max_sync(FULL_MASK, static_cast<unsigned>(gsize));
+#pragma unroll 2
                 for (int it = 1; it < maxsize; ++it) {  // left fold along each group, one link per round
                     const double prev = __shfl_sync(FULL_MASK, v, pred);
                     if (rank == it) v = prev + w;
@@ -989,6 +992,7 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 if (mk > 0) {
                     const double rk = ent[q0.x + lane].y;
                     double v = 0.0;
+#pragma unroll 4
                     for (int i = 0; i < mk; ++i) v += rk;  // mc_engine.cpp:49, chain order
                     const int sl = hash_slot<GL>(sm.keys, cap_mask, shift, tcol[q0.x + lane], nn);
                     if (sl < 0) bad = true;
