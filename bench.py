@@ -548,30 +548,37 @@ def run_ours(args):
         except (OSError, ValueError, KeyError):
             l2_peak = None
         walk_ms_rank0 = walk_ms_local
-        achieved = alg_bytes_local / (walk_ms_rank0 / 1e3) / 1e9 if walk_ms_rank0 > 0 else 0.0
         ncu = load_ncu(args.config, args.rng)
         s0 = stats[-1]
+        # This kernel's algorithmic bytes per walk step: the 32-byte state record,
+        # the 32-byte {cum, ratio} pair its guide bucket points at (16 buckets
+        # resolve nearly every draw there) and the 4-byte column: 68 B (a forced
+        # move reads only the record).  SURVEY §8d's 20 + 8*deg(s) charges the
+        # reference's linear CDF scan and is reported beside it.
+        alg_bytes = 68.0 * steps_local
+        t_walk = walk_ms_rank0 / 1e3 if walk_ms_rank0 > 0 else float("inf")
+        achieved = alg_bytes / t_walk / 1e9
+        model_gbs = alg_bytes_local / t_walk / 1e9
         roofline = {
-            # The walk tables (0.6 GB at C2) stay L2-resident, so L2 is the memory
-            # level the kernel reads from; ncu shows it issue-bound below that
-            # (see "measured").  achieved = SURVEY §8d model bytes / kernel time.
+            # The walk's tables stay L2-resident (ncu: DRAM traffic ~0.3% of the
+            # L2 traffic), so L2 is the memory level it reads; it is bound below
+            # that by SM instruction issue (measured.issue_active).
             "bound": "l2", "kernel": "k_walk", "achieved": achieved, "peak": l2_peak, "unit": "GB/s",
             "frac": (achieved / l2_peak) if l2_peak else None,
             "traffic": ncu["dram_bytes_per_launch"] if ncu else None,
             "peak_source": "profiles/l2_peak.json (tools/l2_peak.cu, L2-resident read kernel on a B200)",
-            "bytes_per_step": "20 + 8*deg(s) (SURVEY.md §8d)", "alg_bytes_per_launch": alg_bytes_local,
-            "walk_kernel_ms": walk_ms_rank0, "hbm_peak": hbm_peak,
+            "bytes_per_step": "68 = 32 B state record + 32 B {cum, ratio} pair at the guide bucket + 4 B column",
+            "alg_bytes_per_launch": alg_bytes, "walk_kernel_ms": walk_ms_rank0, "hbm_peak": hbm_peak,
+            "model_8d": {"bytes_per_step": "20 + 8*deg(s) (SURVEY.md §8d: the reference's full CDF row)",
+                         "bytes_per_launch": alg_bytes_local, "achieved": model_gbs,
+                         "frac_l2": (model_gbs / l2_peak) if l2_peak else None, "frac_hbm": model_gbs / hbm_peak},
             "measured": (dict({k: ncu[k] for k in ("l2_bytes_per_launch", "dram_bytes_per_launch", "issue_active",
                                                    "ipc", "warp_instructions_per_launch", "l1_hit_rate",
                                                    "l2_hit_rate", "captured") if k in ncu},
-                              l2_gbs=ncu["l2_bytes_per_launch"] / (walk_ms_rank0 / 1e3) / 1e9,
-                              l2_frac=(ncu["l2_bytes_per_launch"] / (walk_ms_rank0 / 1e3) / 1e9 / l2_peak)
-                              if l2_peak else None,
-                              dram_frac=ncu["dram_bytes_per_launch"] / (walk_ms_rank0 / 1e3) / 1e9 / hbm_peak)
+                              l2_gbs=ncu["l2_bytes_per_launch"] / t_walk / 1e9,
+                              l2_frac=(ncu["l2_bytes_per_launch"] / t_walk / 1e9 / l2_peak) if l2_peak else None,
+                              dram_frac=ncu["dram_bytes_per_launch"] / t_walk / 1e9 / hbm_peak)
                          if ncu else "no ncu capture of this walk-kernel source (profiles/walk_traffic.json)"),
-            "note": ("the model counts the whole CDF row (8*deg B) per step; the guide table reads ~1-2 "
-                     "entries, so L2 moves ~1/3 of the model bytes (measured.l2_bytes_per_launch) and the "
-                     "kernel is bound by SM instruction issue (measured.issue_active), not by L2 or HBM"),
         }
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
