@@ -253,6 +253,7 @@ void engine_release(mcmi_engine* e) {
 constexpr int kLogMax = 256;         // deposit-log entries per warp (shared memory)
 constexpr int64_t kMaxWalkLen = 1 << 16;  // longest walk (log capacity of the global tier)
 constexpr int64_t kMaxSmemWalkLen = 256;  // longer max_len go straight to the global tier
+constexpr int64_t kLongRowDeposits = 1 << 16;  // N * L from which the pilot fills the GPU
 
 struct Tier {
     int cap, cap_limit, lanes, log_stride, warps_per_block;
@@ -518,6 +519,31 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         st.launches += 1;
         tri = e->tri.as<unsigned char>();
     }
+    // Resident warps of a global-scratch tier: one table per warp, up to 32
+    // warps/SM.  Global-tier tables are latency-bound (random probes into HBM),
+    // so resident warps are throughput: up to half of the free memory, 64 GB
+    // (MCMI_SCRATCH_GB), is scratch.
+    auto global_warps = [&](const Tier& t, int64_t* warps) -> Status {
+        const size_t per_warp = walk_global_bytes_per_warp(t.cap, t.lanes, t.log_stride);
+        const int64_t full = static_cast<int64_t>(e->num_sms) * 32;
+        if (e->gscratch.cap >= static_cast<size_t>(full) * per_warp) {
+            // the scratch already holds every resident warp's table: no
+            // cudaMemGetInfo (it can stall for tens of ms behind the driver)
+            *warps = full;
+            return ok();
+        }
+        static const size_t budget_max = [] {
+            const char* v = getenv("MCMI_SCRATCH_GB");
+            return (v && *v ? static_cast<size_t>(std::max(1, atoi(v))) : size_t{64}) << 30;
+        }();
+        size_t free_b = 0, total_b = 0;
+        MCMI_TRY(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+        const size_t budget = std::min<size_t>(budget_max, (free_b + e->gscratch.cap) / 2);
+        int64_t w = std::min<int64_t>(static_cast<int64_t>(budget / per_warp), full);
+        if (w < 1) return fail(MCMI_ENOMEM, "accumulator row too large for device memory");
+        *warps = std::max<int64_t>(8, w / 8 * 8);
+        return ok();
+    };
     int64_t pool_used = 0;
     int cur = 0;
     unsigned long long total_steps = 0, total_deg = 0;
@@ -572,28 +598,10 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         wa.gscratch = nullptr;
         int64_t max_warps = 0;
         if (t.global) {
+            Status gs = global_warps(t, &max_warps);
+            if (gs.code) return gs;
             const size_t per_warp = walk_global_bytes_per_warp(t.cap, t.lanes, t.log_stride);
-            const int64_t full = static_cast<int64_t>(e->num_sms) * 32;  // 32 warps/SM
-            if (e->gscratch.cap >= static_cast<size_t>(full) * per_warp) {
-                // the scratch already holds every resident warp's table: no
-                // cudaMemGetInfo (it can stall for tens of ms behind the driver)
-                max_warps = full;
-            } else {
-                // Global-tier tables are latency-bound (random probes into HBM),
-                // so resident warps are throughput: up to half of the free
-                // memory, 64 GB (MCMI_SCRATCH_GB), is scratch.  Cached in the engine.
-                static const size_t budget_max = [] {
-                    const char* v = getenv("MCMI_SCRATCH_GB");
-                    return (v && *v ? static_cast<size_t>(std::max(1, atoi(v))) : size_t{64}) << 30;
-                }();
-                size_t free_b = 0, total_b = 0;
-                MCMI_TRY(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
-                const size_t budget = std::min<size_t>(budget_max, (free_b + e->gscratch.cap) / 2);
-                max_warps = std::min<int64_t>(static_cast<int64_t>(budget / per_warp), full);
-                if (max_warps < 1) return fail(MCMI_ENOMEM, "accumulator row too large for device memory");
-                max_warps = std::max<int64_t>(8, max_warps / 8 * 8);
-                MCMI_TRY(e->gscratch.ensure(static_cast<size_t>(max_warps) * per_warp), "alloc accumulator scratch");
-            }
+            MCMI_TRY(e->gscratch.ensure(static_cast<size_t>(max_warps) * per_warp), "alloc accumulator scratch");
             wa.gscratch = e->gscratch.as<unsigned char>();
         }
         wa.stage_col = e->stage_col.as<int>();
@@ -636,7 +644,17 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     // tiers, so results never depend on this choice.
     size_t t0 = 0;
     int64_t pilot_rows = 0;
-    const int64_t pilot = std::min<int64_t>(1024, rows / 4);
+    int64_t pilot = std::min<int64_t>(1024, rows / 4);
+    if (tiers.size() > 1 && deposits >= kLongRowDeposits && tiers.back().global) {
+        // Long rows (C5's wide corners: a row is 10^5+ steps of one warp): the
+        // pilot launch lasts one row however few rows it holds, so it takes as
+        // many as the last tier keeps resident, up to a quarter of the rows
+        // (C5 10^4 x 32: 4 row-latency waves -> 3)
+        int64_t w = 0;
+        Status gs = global_warps(tiers.back(), &w);
+        if (gs.code) return gs;
+        pilot = std::max(pilot, std::min(rows / 4, w));
+    }
     if (tiers.size() > 1 && pilot >= 64) {
         int64_t ovf = 0;
         Status ps = run_tier(tiers.back(), pilot, nullptr, 0, &ovf);

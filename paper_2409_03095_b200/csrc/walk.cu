@@ -231,18 +231,42 @@ __device__ __forceinline__ unsigned long long topk_key(int c, double v, int diag
 // radix select over the 64-bit key (8 passes) and, for ties at the threshold,
 // over the column (4 passes).  Entry i is kept iff key > T || (key == T &&
 // col <= Tc).  hist: 256 scratch words.  O(s) instead of the O(s^2) ranking.
-__device__ void radix_topk(const int* keys, const double* vals, int s, int k, int diag,
-                           unsigned* hist, unsigned long long& T, int& Tc) {
+// After the first pass that leaves fewer than s/2 entries in play (those whose
+// leading bytes equal the threshold's; values of a row usually share the top
+// byte, so typically after the second) they are copied to [s, s + cnt) when at
+// most `spare` fit there, and the later passes read only those (wide rows: 4
+// passes over the row instead of 9);
+// `copied` returns cnt (0 if not copied): those slots must be emptied again.
+__device__ void radix_topk(int* keys, double* vals, int s, int k, int diag, unsigned* hist, int spare,
+                           unsigned long long& T, int& Tc, int& copied) {
     const int lane = static_cast<int>(threadIdx.x & 31);
+    const unsigned lt_mask = (1u << lane) - 1u;
     unsigned long long prefix = 0, mask = 0;
     unsigned need = static_cast<unsigned>(k);
     unsigned eq = 0;  // entries matching the full prefix after the last pass
+    const int* lk = keys;  // the entries scanned by the passes
+    const double* lv = vals;
+    int ln = s;
+    copied = 0;
     for (int shift = 56; shift >= 0; shift -= 8) {
         for (int b = lane; b < 256; b += 32) hist[b] = 0;
         __syncwarp();
-        for (int i = lane; i < s; i += 32) {
-            const unsigned long long key = topk_key(keys[i], vals[i], diag);
-            if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+        // 4 entries per lane in flight: on the global tiers these passes stream
+        // MBs per row from HBM, latency-bound at one load pair per iteration
+        for (int i0 = lane; i0 < ln; i0 += 128) {
+            int kk[4];
+            double vv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int i = i0 + 32 * u;
+                kk[u] = i < ln ? lk[i] : diag;
+                vv[u] = i < ln ? lv[i] : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const unsigned long long key = topk_key(kk[u], vv[u], diag);
+                if (i0 + 32 * u < ln && (key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
+            }
         }
         __syncwarp();
         unsigned c[8], tot = 0;
@@ -282,6 +306,34 @@ __device__ void radix_topk(const int* keys, const double* vals, int s, int k, in
         prefix |= static_cast<unsigned long long>(d) << shift;
         mask |= 0xffull << shift;
         __syncwarp();
+        if (ln == s && shift > 0 && eq <= static_cast<unsigned>(spare) && eq < static_cast<unsigned>(s) / 2) {
+            int o = 0;
+            for (int g0 = 0; g0 < s; g0 += 128) {
+                int kk[4];
+                double vv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = g0 + 32 * u + lane;
+                    kk[u] = i < s ? keys[i] : diag;
+                    vv[u] = i < s ? vals[i] : 0.0;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const bool in = g0 + 32 * u + lane < s && (topk_key(kk[u], vv[u], diag) & mask) == prefix;
+                    const unsigned bal = __ballot_sync(FULL_MASK, in);
+                    if (in) {
+                        keys[s + o + __popc(bal & lt_mask)] = kk[u];
+                        vals[s + o + __popc(bal & lt_mask)] = vv[u];
+                    }
+                    o += __popc(bal);
+                }
+            }
+            __syncwarp();
+            lk = keys + s;
+            lv = vals + s;
+            ln = o;
+            copied = o;
+        }
     }
     T = prefix;
     Tc = INT_MAX;
@@ -290,9 +342,9 @@ __device__ void radix_topk(const int* keys, const double* vals, int s, int k, in
         for (int shift = 24; shift >= 0; shift -= 8) {
             for (int b = lane; b < 256; b += 32) hist[b] = 0;
             __syncwarp();
-            for (int i = lane; i < s; i += 32) {
-                const unsigned col = static_cast<unsigned>(keys[i]);
-                if (topk_key(keys[i], vals[i], diag) == T && (col & cmask) == cprefix)
+            for (int i = lane; i < ln; i += 32) {
+                const unsigned col = static_cast<unsigned>(lk[i]);
+                if (topk_key(lk[i], lv[i], diag) == T && (col & cmask) == cprefix)
                     atomicAdd(&hist[(col >> shift) & 255u], 1u);
             }
             __syncwarp();
@@ -947,12 +999,15 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 const int gsize = ok ? __popc(peers) : 0;
                 const int leader = __ffs(peers) - 1;
                 int slot = 0;
+                bool fresh = false;  // the leader inserted the column: its value is 0.0
                 if (ok && rank == 0) {
                     if (NB && nb) {
                         slot = c;
                         atomicOr(&nb_mask[c >> 5], 1u << (c & 31));
                     } else {
+                        const int had = n_new;
                         slot = hash_slot<GL>(sm.keys, cap_mask, shift, c, n_new);
+                        fresh = n_new != had;
                         if (slot < 0) fail = true;
                     }
                 }
@@ -960,7 +1015,9 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                 else slot = __shfl_sync(FULL_MASK, slot, leader);
                 const double w = ok ? sm.log_w[LF == 2 ? lf2_w_at(tq, j) : q] : 0.0;
                 double v = w;
-                if (ok && rank == 0 && slot >= 0) v = sm.vals[slot] + w;
+                // an empty slot holds 0.0 (the accumulator invariant): a fresh
+                // column skips the load (HBM latency on the global tiers)
+                if (ok && rank == 0 && slot >= 0) v = (GL && fresh ? 0.0 : sm.vals[slot]) + w;
                 const int maxsize = __reduce_max_sync(FULL_MASK, static_cast<unsigned>(gsize));
 #pragma unroll 2
                 for (int it = 1; it < maxsize; ++it) {  // left fold along each group, one link per round
@@ -1029,35 +1086,59 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
         // ------------------------------------------------------ finalize
         // compact occupied slots to [0, s) in place, emptying the vacated slots
         int o = 0;
-        for (int i0 = 0; i0 < cap; i0 += 32) {
-            const int i = i0 + lane;
-            const int kk = sm.keys[i];
-            const double vv = sm.vals[i];
-            bool occ = kk != EMPTY_KEY;
-            bool drop = false;  // NB: pre-inserted but never visited
-            if (NB && nb) {
-                const unsigned wbits = __shfl_sync(FULL_MASK, nb_bits, i0 >> 5);
-                drop = occ && !((wbits >> lane) & 1u);
-                occ = occ && !drop;
+        // GL: 4 chunks of slots loaded per round (HBM latency); the writes of a
+        // round go to slots that round (or an earlier one) already read
+        constexpr int CU = GL ? 4 : 1;
+        for (int g0 = 0; g0 < cap; g0 += 32 * CU) {
+            int kk[CU];
+            double vv[CU];
+#pragma unroll
+            for (int u = 0; u < CU; ++u) {
+                const int i = g0 + 32 * u + lane;
+                kk[u] = i < cap ? sm.keys[i] : EMPTY_KEY;
+                vv[u] = i < cap ? sm.vals[i] : 0.0;
             }
-            const unsigned bal = __ballot_sync(FULL_MASK, occ);
-            const int dst = o + __popc(bal & lt_mask);
-            __syncwarp();
-            if ((occ && dst != i) || drop) {
-                sm.keys[i] = EMPTY_KEY;
-                sm.vals[i] = 0.0;
+#pragma unroll
+            for (int u = 0; u < CU; ++u) {
+                const int i0 = g0 + 32 * u;
+                const int i = i0 + lane;
+                bool occ = kk[u] != EMPTY_KEY;
+                bool drop = false;  // NB: pre-inserted but never visited
+                if (NB && nb) {
+                    const unsigned wbits = __shfl_sync(FULL_MASK, nb_bits, i0 >> 5);
+                    drop = occ && !((wbits >> lane) & 1u);
+                    occ = occ && !drop;
+                }
+                const unsigned bal = __ballot_sync(FULL_MASK, occ);
+                const int dst = o + __popc(bal & lt_mask);
+                __syncwarp();
+                if ((occ && dst != i) || drop) {
+                    sm.keys[i] = EMPTY_KEY;
+                    sm.vals[i] = 0.0;
+                }
+                __syncwarp();
+                if (occ) {
+                    sm.keys[dst] = kk[u];
+                    sm.vals[dst] = vv[u];
+                }
+                o += __popc(bal);
+                __syncwarp();
             }
-            __syncwarp();
-            if (occ) {
-                sm.keys[dst] = kk;
-                sm.vals[dst] = vv;
-            }
-            o += __popc(bal);
-            __syncwarp();
         }
         const int s = distinct;
         const double inv_n = 1.0 / static_cast<double>(chains_run);  // mc_engine.cpp:109
-        for (int i = lane; i < s; i += 32) sm.vals[i] = sm.vals[i] * inv_n;
+        if (GL) {
+            for (int g0 = lane; g0 < s; g0 += 128) {
+                double vv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) vv[u] = g0 + 32 * u < s ? sm.vals[g0 + 32 * u] : 0.0;
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (g0 + 32 * u < s) sm.vals[g0 + 32 * u] = vv[u] * inv_n;
+            }
+        } else {
+            for (int i = lane; i < s; i += 32) sm.vals[i] = sm.vals[i] * inv_n;
+        }
         __syncwarp();
 
         const int64_t kret = a.retain_k;
@@ -1068,30 +1149,40 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
             // retain_top_k by radix selection, then sort only the kept entries
             unsigned* hist = reinterpret_cast<unsigned*>(sm.vals + (cap - 128));  // free: s <= 3/4 cap
             unsigned long long T;
-            int Tc;
-            radix_topk(sm.keys, sm.vals, s, static_cast<int>(kret), rowc, hist, T, Tc);
+            int Tc, copied;
+            radix_topk(sm.keys, sm.vals, s, static_cast<int>(kret), rowc, hist, cap - 128 - s, T, Tc, copied);
             for (int b = lane; b < 256; b += 32) hist[b] = 0;  // restore the zeros of the vals array
+            for (int i = s + lane; i < s + copied; i += 32) {  // and empty the candidates' copies
+                sm.keys[i] = EMPTY_KEY;
+                sm.vals[i] = 0.0;
+            }
             __syncwarp();
             int kept = 0;
-            for (int i0 = 0; i0 < s; i0 += 32) {  // stable forward compaction of the kept set
-                const int i = i0 + lane;
-                int kk = 0;
-                double vv = 0.0;
-                bool keep = false;
-                if (i < s) {
-                    kk = sm.keys[i];
-                    vv = sm.vals[i];
-                    const unsigned long long key = topk_key(kk, vv, rowc);
-                    keep = key > T || (key == T && kk <= Tc);
+            for (int g0 = 0; g0 < s; g0 += 128) {  // stable forward compaction of the kept set
+                int kk[4];
+                double vv[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int i = g0 + 32 * u + lane;
+                    kk[u] = i < s ? sm.keys[i] : rowc;
+                    vv[u] = i < s ? sm.vals[i] : 0.0;
                 }
-                const unsigned bal = __ballot_sync(FULL_MASK, keep);
-                __syncwarp();
-                if (keep) {
-                    sm.keys[kept + __popc(bal & lt_mask)] = kk;
-                    sm.vals[kept + __popc(bal & lt_mask)] = vv;
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    bool keep = false;
+                    if (g0 + 32 * u + lane < s) {
+                        const unsigned long long key = topk_key(kk[u], vv[u], rowc);
+                        keep = key > T || (key == T && kk[u] <= Tc);
+                    }
+                    const unsigned bal = __ballot_sync(FULL_MASK, keep);
+                    __syncwarp();
+                    if (keep) {
+                        sm.keys[kept + __popc(bal & lt_mask)] = kk[u];
+                        sm.vals[kept + __popc(bal & lt_mask)] = vv[u];
+                    }
+                    kept += __popc(bal);
+                    __syncwarp();
                 }
-                kept += __popc(bal);
-                __syncwarp();
             }
             len = kept;
             keep_all = true;

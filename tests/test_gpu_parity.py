@@ -290,6 +290,29 @@ def test_global_tier_and_radix_topk(mc, oracle_mod, ref_mod, rng, k):
 
 
 @pytest.mark.parametrize("rng", [0, 1])
+@pytest.mark.parametrize("k", [100, 300])
+def test_radix_topk_ties_on_global_tier(mc, oracle_mod, rng, k):
+    # 3D Laplacian, 10-step walks: 258-571 distinct columns per row on the
+    # global-scratch tiers, whose values repeat (every step-t deposit of an
+    # interior path carries the same weight), so retain_top_k cuts through ties
+    # (30 of the 64 rows at k = 300) and the radix selection's column passes
+    # run on the copied candidates
+    from paper_2409_03095_b200 import generators as G
+    g = G.laplacian3d(16)
+    b = mc.CsrMatrix(g.n, g.row_ptr, g.col_idx, g.values)
+    cfg = mc.McConfig(alpha=0.5, delta=1e-300, chains_override=1000, max_len_override=10, retain_k=k,
+                      master_seed=3, rng_mode=rng)
+    inv = mc.compute_preconditioner(b, cfg, rows=(1800, 1864))
+    want = oracle_mod.compute_preconditioner(b.n, b.row_ptr, b.col_idx, b.values, row_begin=1800, row_end=1864,
+                                             **cfg.oracle_kwargs())
+    assert want.entries_before.max() > 256
+    assert np.array_equal(inv.m.row_ptr, want.row_ptr)
+    assert np.array_equal(inv.m.col_idx, want.col_idx)
+    assert bits_equal(inv.m.values, want.values)
+    assert np.array_equal(inv.row_meta.entries_before_retention, want.entries_before)
+
+
+@pytest.mark.parametrize("rng", [0, 1])
 def test_radix_topk_midsize_rows(mc, oracle_mod, rng):
     # 300-1700 distinct columns per row with retain_k = 32: the shared-memory
     # tiers with radix selection (rows > 256 entries)

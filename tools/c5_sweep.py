@@ -30,6 +30,7 @@ def main():
     p.add_argument("--rng", default="reference", choices=["reference", "keyed"])
     p.add_argument("--chains", default="100,1000,10000,100000")
     p.add_argument("--lens", default="4,8,16,32,64")
+    p.add_argument("--hash", action="store_true", help="print the sha256 (16 hex) of the timed build's M")
     a = p.parse_args()
     from paper_2409_03095_b200 import generators as G
     from paper_2409_03095_b200.engine import DeviceEngine
@@ -48,6 +49,13 @@ def main():
             eng.build(b.n, rp, ci, v, cfg, 0, min(rows, 64))  # warm-up (tier scratch allocation)
             d = eng.build(b.n, rp, ci, v, cfg, 0, rows)
             st = d.stats
+            msha = None
+            if a.hash:
+                import hashlib
+                h = hashlib.sha256()
+                for t in eng.to_tensors(d)[:3]:
+                    h.update(t.cpu().numpy().tobytes())
+                msha = h.hexdigest()[:16]
             ok = None
             if a.check:
                 from oracle import oracle
@@ -62,7 +70,7 @@ def main():
                               "ms_total": round(st["ms_total"], 3), "ms_walk_kernel": round(st["ms_walk_kernel"], 3),
                               "steps_per_s": st["walk_steps"] / (st["ms_total"] / 1e3),
                               "hash_cap": st["hash_cap"], "rows_retried": st["rows_retried"], "nnz_M": st["nnz"],
-                              "exact_vs_oracle": ok, "rng": a.rng, "gen_s": round(gen_s, 1)}), flush=True)
+                              "exact_vs_oracle": ok, "m_sha16": msha, "rng": a.rng, "gen_s": round(gen_s, 1)}), flush=True)
     eng.close()
 
 
