@@ -253,7 +253,7 @@ void engine_release(mcmi_engine* e) {
 constexpr int kLogMax = 256;         // deposit-log entries per warp (shared memory)
 constexpr int64_t kMaxWalkLen = 1 << 16;  // longest walk (log capacity of the global tier)
 constexpr int64_t kMaxSmemWalkLen = 256;  // longer max_len go straight to the global tier
-constexpr int64_t kLongRowDeposits = 1 << 16;  // N * L from which the pilot fills the GPU
+constexpr int64_t kLongRowDeposits = 1 << 15;  // N * L from which the pilot sizes by waves
 
 struct Tier {
     int cap, cap_limit, lanes, log_stride, warps_per_block;
@@ -646,14 +646,20 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     int64_t pilot_rows = 0;
     int64_t pilot = std::min<int64_t>(1024, rows / 4);
     if (tiers.size() > 1 && deposits >= kLongRowDeposits && tiers.back().global) {
-        // Long rows (C5's wide corners: a row is 10^5+ steps of one warp): the
-        // pilot launch lasts one row however few rows it holds, so it takes as
-        // many as the last tier keeps resident, up to a quarter of the rows
-        // (C5 10^4 x 32: 4 row-latency waves -> 3)
+        // Long rows (C5's wide corners: a row is 10^5+ steps of one warp): a
+        // launch lasts a whole number of row latencies (waves of resident
+        // warps) however few rows its last wave holds, so the pilot takes the
+        // remainder rows % W of W resident warps (all rows when they fit one
+        // wave) and the rest run in full waves (C5 10^4 x 32: 4 waves -> 3,
+        // 10^5 x 32: 2 -> 1)
         int64_t w = 0;
         Status gs = global_warps(tiers.back(), &w);
         if (gs.code) return gs;
-        pilot = std::max(pilot, std::min(rows / 4, w));
+        const int64_t r = rows % w;
+        pilot = rows <= w ? rows : (r >= 64 ? r : w);
+        // the pilot's output stays staged until its chunk is assembled
+        const int64_t staged = staging_budget_bytes() / (stride_of(tiers.back()) * 12);
+        pilot = std::max<int64_t>(std::min<int64_t>(1024, rows / 4), std::min(pilot, staged));
     }
     if (tiers.size() > 1 && pilot >= 64) {
         int64_t ovf = 0;

@@ -313,6 +313,25 @@ def test_radix_topk_ties_on_global_tier(mc, oracle_mod, rng, k):
 
 
 @pytest.mark.parametrize("rng", [0, 1])
+def test_long_rows_pilot_takes_the_wave(mc, oracle_mod, ref_mod, rng):
+    # N*L = 72,000 deposits per row (>= 2^15, engine.cu kLongRowDeposits): the
+    # pilot sizing for long rows; 64 rows fit one wave, so the pilot launch on
+    # the last tier builds them all
+    rb = ref_mod.gen_broad_spectrum(8192, 24, 1e-4, 1.0, 3)
+    b = mc.CsrMatrix(rb.n, rb.row_ptr, rb.col_idx, rb.values)
+    cfg = mc.McConfig(alpha=1.2, delta=1e-300, chains_override=12000, max_len_override=6, retain_k=32,
+                      master_seed=17, rng_mode=rng)
+    inv = mc.compute_preconditioner(b, cfg, rows=(100, 164))
+    want = oracle_mod.compute_preconditioner(b.n, b.row_ptr, b.col_idx, b.values, row_begin=100, row_end=164,
+                                             **cfg.oracle_kwargs())
+    assert np.array_equal(inv.m.row_ptr, want.row_ptr)
+    assert np.array_equal(inv.m.col_idx, want.col_idx)
+    assert bits_equal(inv.m.values, want.values)
+    assert np.array_equal(inv.row_meta.entries_before_retention, want.entries_before)
+    assert np.array_equal(inv.row_meta.chains_used, want.chains_used)
+
+
+@pytest.mark.parametrize("rng", [0, 1])
 def test_radix_topk_midsize_rows(mc, oracle_mod, rng):
     # 300-1700 distinct columns per row with retain_k = 32: the shared-memory
     # tiers with radix selection (rows > 256 entries)
