@@ -651,12 +651,14 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         // warps) however few rows its last wave holds, so the pilot takes the
         // remainder rows % W of W resident warps (all rows when they fit one
         // wave) and the rest run in full waves (C5 10^4 x 32: 4 waves -> 3,
-        // 10^5 x 32: 2 -> 1)
+        // 10^5 x 64: 2 -> 1)
         int64_t w = 0;
         Status gs = global_warps(tiers.back(), &w);
         if (gs.code) return gs;
+        // (only for a few waves: at 10^4 x 16, 5.3 waves, the larger pilot on
+        // the bound-sized tier cost more than the partial wave it saved, +7%)
         const int64_t r = rows % w;
-        pilot = rows <= w ? rows : (r >= 64 ? r : w);
+        if (rows <= 3 * w) pilot = rows <= w ? rows : (r >= 64 ? r : w);
         // the pilot's output stays staged until its chunk is assembled
         const int64_t staged = staging_budget_bytes() / (stride_of(tiers.back()) * 12);
         pilot = std::max<int64_t>(std::min<int64_t>(1024, rows / 4), std::min(pilot, staged));
