@@ -512,6 +512,36 @@ def test_neighbourhood_slot_tables_match_plain_kernel(mc, oracle_mod, rng, over,
         assert np.array_equal(nbk.row_meta.entries_before_retention[lo:hi], want.entries_before)
 
 
+@pytest.mark.parametrize("rng", [0, 1])
+def test_neighbourhood_tables_zero_sum_columns(mc, oracle_mod, rng):
+    """27-point stencil with off-diagonals of magnitude 1 and random signs:
+    every interior transition has the same |ratio|, so 2-step deposits are
+    +-R^2 and a column's sum often cancels to exactly 0.0.  Such a column was
+    visited: it counts in entries_before (then is pruned from M), which the
+    tables' visited marks must get right."""
+    import os
+    from paper_2409_03095_b200 import generators as G
+    g = G.stencil27(12, 12, 12, seed=4)
+    r = np.random.default_rng(7)
+    v = np.where(r.random(g.values.size) < 0.5, -1.0, 1.0)
+    rows = np.repeat(np.arange(g.n), np.diff(g.row_ptr))
+    v[g.col_idx == rows] = 30.0
+    b = mc.CsrMatrix(g.n, g.row_ptr, g.col_idx, v)
+    cfg = mc.McConfig(rng_mode=rng, chains_override=3000, max_len_override=2, alpha=0.5)
+    os.environ["MCMI_WALK_NB"] = "1"
+    try:
+        nbk = mc.compute_preconditioner(b, cfg)
+    finally:
+        del os.environ["MCMI_WALK_NB"]
+    lo, hi = 600, 680
+    want = oracle_mod.compute_preconditioner(b.n, b.row_ptr, b.col_idx, b.values, row_begin=lo, row_end=hi,
+                                             **cfg.oracle_kwargs())
+    assert (want.entries_before > np.diff(want.row_ptr)).any()  # zero sums pruned after counting
+    a, z = nbk.m.row_ptr[lo], nbk.m.row_ptr[hi]
+    assert np.array_equal(nbk.m.col_idx[a:z], want.col_idx) and bits_equal(nbk.m.values[a:z], want.values)
+    assert np.array_equal(nbk.row_meta.entries_before_retention[lo:hi], want.entries_before)
+
+
 def _mixed_triangle_matrix(mc, n=400, seed=3):
     """Rows with and without triangles through them: a ring (triangle-free)
     plus random chords, some closing triangles; degrees 2..8."""
