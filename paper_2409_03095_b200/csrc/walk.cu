@@ -81,6 +81,17 @@ __device__ __forceinline__ void ldg256(const void* p, uint4& lo, uint4& hi) {
                  : "l"(p));
 }
 
+// Two consecutive 16-byte {cum, ratio} entries from a 32-byte-aligned address
+// in one load.
+__device__ __forceinline__ void ldg_pair(const double2* p, double2& a, double2& b) {
+    uint4 lo, hi;
+    ldg256(p, lo, hi);
+    a = make_double2(__hiloint2double(static_cast<int>(lo.y), static_cast<int>(lo.x)),
+                     __hiloint2double(static_cast<int>(lo.w), static_cast<int>(lo.z)));
+    b = make_double2(__hiloint2double(static_cast<int>(hi.y), static_cast<int>(hi.x)),
+                     __hiloint2double(static_cast<int>(hi.w), static_cast<int>(hi.z)));
+}
+
 // Insert-or-find; returns the slot or -1 if the table is full.  The key's home
 // slot h is probed first (one 4-byte load: most lookups end there, hit or
 // empty); past an occupied home slot the probe continues over 4-slot buckets
@@ -547,6 +558,16 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
     const int B = LF ? 32 : a.lanes;            // chains per batch
     const int logn = LF ? round32(32 * LF) : a.log_n;  // round32(B * S), host-computed (kernel parameter)
     constexpr bool kTF = split_fold_kernel<LF, NB>();
+    // Aligned 32-byte pair loads in the neighbourhood-table kernels (C2 at
+    // eps = 0.01, where the L1 data pipe binds: -1.2% reference stream, -2.4%
+    // keyed); the other kernels keep two 16-byte loads (C3 +4%, C4 +4% with
+    // the aligned form: more spills).  Loading the pair's two columns with it
+    // (one 8-byte load) measured no better.
+#ifdef MCMI_PAIR_ALL
+    constexpr bool kAlignedPair = true;
+#else
+    constexpr bool kAlignedPair = NB;
+#endif
     const size_t per_warp = (LF && CAPC) ? static_cast<size_t>(CAPC + logn) * 12 + (NB ? kNbBytes : 0) +
                                                (kTF ? kTfBytes : 0)
                                          : static_cast<size_t>(a.warp_bytes) + (kTF ? kTfBytes : 0);
@@ -785,14 +806,30 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                     const unsigned gw = mb < 8 ? (mb < 4 ? r0.z : r0.w) : (mb < 12 ? r1.x : r1.y);
                     const unsigned g = (gw >> ((mb & 3) * 8)) & 0xffu;
                     unsigned q = r0.x + g * r1.w;  // r1.w = guide scale ceil(deg / 255)
-                    // the first pair resolves almost every draw (16 guide buckets):
-                    // selects, not a loop, in the common case
-                    double2 e0 = ent[q];
-                    double2 e1 = ent[q + 1];  // past the row only when e0 is its +inf entry
-                    while (!(u < e0.x) && !(u < e1.x)) {
-                        q += 2;
+                    double2 e0, e1;
+                    if (kAlignedPair) {
+                        // Entry pairs are read as one aligned 32-byte load from the
+                        // even index at or below the guide start (one L1 request per
+                        // pair instead of two).  Starting one entry early is exact:
+                        // that entry has cum <= m/16 <= u, or, when it is the
+                        // previous row's last entry (odd row begin), it is masked out.
+                        q &= ~1u;
+                        ldg_pair(ent + q, e0, e1);
+                        if (q < r0.x) e0.x = -1.0;  // not this row's: u < -1 is false
+                        while (!(u < e0.x) && !(u < e1.x)) {
+                            q += 2;
+                            ldg_pair(ent + q, e0, e1);
+                        }
+                    } else {
+                        // the first pair resolves almost every draw (16 guide
+                        // buckets): selects, not a loop, in the common case
                         e0 = ent[q];
-                        e1 = ent[q + 1];
+                        e1 = ent[q + 1];  // past the row only when e0 is its +inf entry
+                        while (!(u < e0.x) && !(u < e1.x)) {
+                            q += 2;
+                            e0 = ent[q];
+                            e1 = ent[q + 1];
+                        }
                     }
                     const bool first_of_pair = u < e0.x;
                     const unsigned k = first_of_pair ? q : q + 1;
