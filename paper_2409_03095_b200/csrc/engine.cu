@@ -647,18 +647,15 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     int64_t pilot = std::min<int64_t>(1024, rows / 4);
     if (tiers.size() > 1 && deposits >= kLongRowDeposits && tiers.back().global) {
         // Long rows (C5's wide corners: a row is 10^5+ steps of one warp): a
-        // launch lasts a whole number of row latencies (waves of resident
-        // warps) however few rows its last wave holds, so the pilot takes the
-        // remainder rows % W of W resident warps (all rows when they fit one
-        // wave) and the rest run in full waves (C5 10^4 x 32: 4 waves -> 3,
-        // 10^5 x 64: 2 -> 1)
+        // launch lasts a whole number of row latencies (waves of W resident
+        // warps) however few rows its last wave holds.  All rows in one wave
+        // when they fit (10^5 x 64: 2 launches -> 1); otherwise the pilot
+        // fills up to a wave, at most a quarter of the rows (10^4 x 32: 4 row
+        // latencies -> 3; 10^4 x 16: 563 -> 521 ms against a 1024-row pilot).
         int64_t w = 0;
         Status gs = global_warps(tiers.back(), &w);
         if (gs.code) return gs;
-        // (only for a few waves: at 10^4 x 16, 5.3 waves, the larger pilot on
-        // the bound-sized tier cost more than the partial wave it saved, +7%)
-        const int64_t r = rows % w;
-        if (rows <= 3 * w) pilot = rows <= w ? rows : (r >= 64 ? r : w);
+        pilot = rows <= w ? rows : std::max(pilot, std::min(rows / 4, w));
         // the pilot's output stays staged until its chunk is assembled
         const int64_t staged = staging_budget_bytes() / (stride_of(tiers.back()) * 12);
         pilot = std::max<int64_t>(std::min<int64_t>(1024, rows / 4), std::min(pilot, staged));
