@@ -525,7 +525,7 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
     // (MCMI_SCRATCH_GB), is scratch.
     auto global_warps = [&](const Tier& t, int64_t* warps) -> Status {
         const size_t per_warp = walk_global_bytes_per_warp(t.cap, t.lanes, t.log_stride);
-        const int64_t full = static_cast<int64_t>(e->num_sms) * 32;
+        const int64_t full = static_cast<int64_t>(e->num_sms) * kGlWarpsPerSm;
         if (e->gscratch.cap >= static_cast<size_t>(full) * per_warp) {
             // the scratch already holds every resident warp's table: no
             // cudaMemGetInfo (it can stall for tens of ms behind the driver)

@@ -185,6 +185,13 @@ cudaError_t launch_transition_probabilities(const int64_t* rp, const int64_t* ci
 cudaError_t launch_count_quantile(const TableBuildArgs& a, int64_t nnz, int64_t n_drop,
                                   void* scratch, size_t scratch_bytes, cudaStream_t s);
 size_t count_quantile_scratch_bytes(int64_t nnz);
+// Global-tier walk kernels: __launch_bounds__(256, kGlMinBlocks), so up to
+// 8 * kGlMinBlocks resident warps per SM (one accumulator table each).
+#ifndef MCMI_GL_MINB
+#define MCMI_GL_MINB 4
+#endif
+constexpr int kGlMinBlocks = MCMI_GL_MINB;
+constexpr int kGlWarpsPerSm = 8 * kGlMinBlocks;
 size_t walk_smem_bytes_per_warp(int cap, int lanes, int log_stride);
 size_t walk_global_bytes_per_warp(int cap, int lanes, int log_stride);
 cudaError_t launch_walk(const WalkArgs& a, int warps_per_block, int num_sms, bool global_tier,

@@ -1409,15 +1409,15 @@ cudaError_t launch_walk(const WalkArgs& a_in, int warps_per_block, int num_sms, 
     // variants: the global tier and the statistics build use one launch bound
     if (mode == 2) {
         if (global_tier)
-            return a.deg_stats ? launch_walk_t<2, 4, true, true>(a, warps_per_block, num_sms, max_warps, s)
-                               : launch_walk_t<2, 4, true, false>(a, warps_per_block, num_sms, max_warps, s);
+            return a.deg_stats ? launch_walk_t<2, kGlMinBlocks, true, true>(a, warps_per_block, num_sms, max_warps, s)
+                               : launch_walk_t<2, kGlMinBlocks, true, false>(a, warps_per_block, num_sms, max_warps, s);
         if (a.deg_stats) return launch_walk_t<2, 6, false, true>(a, warps_per_block, num_sms, 0, s);
         return launch_walk_t<2, 6, false, false>(a, warps_per_block, num_sms, 0, s);
     }
     if (mode == 0) {
         if (global_tier)
-            return a.deg_stats ? launch_walk_t<0, 4, true, true>(a, warps_per_block, num_sms, max_warps, s)
-                               : launch_walk_t<0, 4, true, false>(a, warps_per_block, num_sms, max_warps, s);
+            return a.deg_stats ? launch_walk_t<0, kGlMinBlocks, true, true>(a, warps_per_block, num_sms, max_warps, s)
+                               : launch_walk_t<0, kGlMinBlocks, true, false>(a, warps_per_block, num_sms, max_warps, s);
         if (a.deg_stats) return launch_walk_t<0, 6, false, true>(a, warps_per_block, num_sms, 0, s);
         if (mb == 5) return launch_walk_t<0, 5, false, false>(a, warps_per_block, num_sms, 0, s);
         if (mb == 4) return launch_walk_t<0, 4, false, false>(a, warps_per_block, num_sms, 0, s);
@@ -1425,8 +1425,8 @@ cudaError_t launch_walk(const WalkArgs& a_in, int warps_per_block, int num_sms, 
         return launch_walk_t<0, 6, false, false>(a, warps_per_block, num_sms, 0, s);
     }
     if (global_tier)
-        return a.deg_stats ? launch_walk_t<1, 4, true, true>(a, warps_per_block, num_sms, max_warps, s)
-                           : launch_walk_t<1, 4, true, false>(a, warps_per_block, num_sms, max_warps, s);
+        return a.deg_stats ? launch_walk_t<1, kGlMinBlocks, true, true>(a, warps_per_block, num_sms, max_warps, s)
+                           : launch_walk_t<1, kGlMinBlocks, true, false>(a, warps_per_block, num_sms, max_warps, s);
     if (a.deg_stats) return launch_walk_t<1, 6, false, true>(a, warps_per_block, num_sms, 0, s);
     if (mb == 5) return launch_walk_t<1, 5, false, false>(a, warps_per_block, num_sms, 0, s);
     if (mb == 4) return launch_walk_t<1, 4, false, false>(a, warps_per_block, num_sms, 0, s);
