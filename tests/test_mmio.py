@@ -290,3 +290,33 @@ def test_cpp_dropin_io():
     r = subprocess.run([exe, "--io-only"], capture_output=True, text=True, timeout=120)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "FAIL" not in r.stdout
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["ddm80_drop_value", "broad200_quantile_k10", "tridiag_longwalk", "poisson2d_100_default_seed0"])
+def test_cli_pipeline_through_library_mm_io_on_gpu(name):
+    """The reference CLI's `precondition` path end to end on the library:
+    B written and read back by the library's Matrix Market code (text
+    byte-identical to the reference writer's), M built on the GPU, M written
+    by the library's writer: its sha256 equals the one recorded from the
+    unmodified reference (tests/golden/make_goldens.py)."""
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from helpers import golden_input, goldens
+    from paper_2409_03095_b200 import mcspai as mc
+    import hashlib
+    case = goldens()[name]
+    n, rp, ci, v = golden_input(case["input"])
+    b = CsrMatrix(n, rp, ci, v)
+    text = mm.format_matrix_market(b)
+    assert text == ref.format_mm(ref.Csr(n, rp, ci, v))
+    b2 = mm.parse_matrix_market(text)
+    assert same(b2, ref.parse_mm(text))
+    d = dict(case["config"])
+    for k in ("mode", "drop_mode", "rng_mode"):
+        if k in d:
+            d[k] = int(d[k])
+    inv = mc.compute_preconditioner(b2, mc.McConfig(**d))
+    out = mm.format_matrix_market(inv.m)
+    assert hashlib.sha256(out).hexdigest() == case["mm_sha256"]
