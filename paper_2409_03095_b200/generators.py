@@ -182,5 +182,9 @@ CONFIGS = {
     "c5_powerlaw_4m": (lambda: powerlaw(4_000_000),
                        {"alpha": 0.1, "delta": 1e-300, "chains_override": 100, "max_len_override": 8,
                         "retain_k": 32}),
+    # the C5 grid's wide corner (bench.py builds its leading 12,500 rows)
+    "c5_powerlaw_4m_1e4x32": (lambda: powerlaw(4_000_000),
+                              {"alpha": 0.1, "delta": 1e-300, "chains_override": 10000, "max_len_override": 32,
+                               "retain_k": 32}),
 }
 
