@@ -586,7 +586,11 @@ Status engine_build(mcmi_engine* e, const mcmi_csr_view& b, const mcmi_config& c
         wa.lanes = t.lanes;
         wa.log_stride = t.log_stride;
         wa.log_magic = static_cast<unsigned>((0x100000000ull + t.log_stride - 1) / t.log_stride);
-        wa.ell0 = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(L, 2)));
+        // reference stream: the first window's speculative stride.  Chains that
+        // run to L draw L times (C5: every chain), so short walks start at L
+        // (C5 10^2 x 8..64 -13..15% against 2); a row whose chains stop early
+        // loses one window and goes dense.
+        wa.ell0 = static_cast<int>(std::max<int64_t>(1, L <= 64 ? L : 2));
         wa.deg_stats = (cfg.flags & MCMI_FLAG_DEG_STATS) ? 1 : 0;
         wa.unscaled = (cfg.flags & MCMI_FLAG_UNSCALED) ? 1 : 0;
         // Neighbourhood slot tables (walk.cu, L = 2): their per-row set-up costs

@@ -706,7 +706,10 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
         unsigned long long row_steps = 0, row_deg = 0;
         // reference-stream speculation state
         PosT D = 0;
-        unsigned ell = LF ? static_cast<unsigned>(LF < 2 ? LF : 2) : static_cast<unsigned>(a.ell0);
+        // first window's stride: L (chains that run to L draw L times; C5's
+        // never stop early, C3-heavy's rarely), not 2, which under-delivered
+        // and sent the first window of every row dense (C5 10^2 x 32 -15%)
+        unsigned ell = LF ? static_cast<unsigned>(LF) : static_cast<unsigned>(a.ell0);
         bool row_done = false;
 
         while (!row_done) {
