@@ -745,7 +745,8 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
 #pragma unroll
             for (int t = 0; LF ? (t < LF) : __any_sync(FULL_MASK, alive); ++t) {
                 if (LF) {  // compile-time trip count: no log overflow, no length test
-                    if (!__any_sync(FULL_MASK, alive)) break;
+                    // (at t = 0 lane 0 is always alive: a batch starts only with chains left)
+                    if (t > 0 && !__any_sync(FULL_MASK, alive)) break;
                 } else {
                     if (alive && t >= L) alive = false;
                     if (alive && m >= S) {
@@ -875,7 +876,8 @@ __global__ void __launch_bounds__(256, MINB) k_walk(const WalkArgs a) {
                     else if (m <= 32) retm |= 1u << (m - 1);
                     else ret_hi = true;
                 }
-                if (fabs(w) < a.delta) alive = false;  // mc_engine.cpp:97
+                // mc_engine.cpp:97 (the last step of a compile-time-L walk needs no test)
+                if (!(LF && t == LF - 1) && fabs(w) < a.delta) alive = false;
             }
 
             if (LF) {  // end-of-chain sentinels for the fold: predicated stores, no loop
